@@ -1,0 +1,97 @@
+#!/usr/bin/env python3
+"""Write tests/golden/verify_<N>.json by running the CPU ORACLE only.
+
+Results over disjoint ranges compose (counts and hist add, max_pmin takes the
+max with the smallest n, first_unresolved_n the min, chk adds mod 2^64), so the
+range [4, N] is computed in pieces of `--piece` integers and each finished piece
+is appended to a resumable JSONL cache.  Nothing here touches the CUDA path:
+every stored value comes from oracle/ (see the oracle's header for citations).
+
+usage: python scripts/make_golden.py --N 1e12 [--threads 6] [--piece 1e10]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from oracle import oracle  # noqa: E402
+
+U64 = (1 << 64) - 1
+
+
+def merge(a, b):
+    if a is None:
+        return dict(b)
+    out = dict(a)
+    for k in ("evens", "verified", "fastpath_unresolved", "unresolved", "sum_pmin"):
+        out[k] = a[k] + b[k]
+    out["chk"] = (a["chk"] + b["chk"]) & U64
+    out["first_unresolved_n"] = min(a["first_unresolved_n"], b["first_unresolved_n"])
+    if (b["max_pmin"], -b["max_pmin_n"]) > (a["max_pmin"], -a["max_pmin_n"]):
+        out["max_pmin"], out["max_pmin_n"] = b["max_pmin"], b["max_pmin_n"]
+    h = dict(a["hist"])
+    for i, c in b["hist"].items():
+        h[i] = h.get(i, 0) + c
+    out["hist"] = h
+    return out
+
+
+def to_json_result(r):
+    d = {k: r[k] for k in oracle.FIELDS}
+    d["hist"] = {str(i): int(c) for i, c in enumerate(r["hist"]) if c}
+    return d
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--N", type=float, required=True)
+    ap.add_argument("--threads", type=int, default=oracle.default_threads())
+    ap.add_argument("--piece", type=float, default=1e10)
+    ap.add_argument("--p-fast", type=int, default=65521)
+    args = ap.parse_args()
+    N = int(args.N)
+    piece = int(args.piece)
+    tag = f"{N:.0e}".replace("+", "")
+    cache = os.path.join(ROOT, "tests", "golden", f".cache_verify_{tag}.jsonl")
+    outp = os.path.join(ROOT, "tests", "golden", f"verify_{tag}.json")
+    done = {}
+    if os.path.exists(cache):
+        with open(cache) as f:
+            for line in f:
+                rec = json.loads(line)
+                done[(rec["lo"], rec["hi"])] = rec
+    total = None
+    t_all = 0.0
+    lo = 4
+    while lo < N + 1:
+        hi = min(lo + piece, N + 1)
+        if (lo, hi) not in done:
+            t0 = time.time()
+            r, _ = oracle.verify(lo, hi, p_fast=args.p_fast, threads=args.threads)
+            dt = time.time() - t0
+            rec = {"lo": lo, "hi": hi, "seconds": dt, "threads": args.threads,
+                   "result": to_json_result(r)}
+            with open(cache, "a") as f:
+                f.write(json.dumps(rec) + "\n")
+            done[(lo, hi)] = rec
+            print(f"[{lo}, {hi}) {dt:.1f}s", flush=True)
+        rec = done[(lo, hi)]
+        t_all += rec["seconds"]
+        res = dict(rec["result"])
+        res["hist"] = {int(k): v for k, v in res["hist"].items()}
+        total = merge(total, res)
+        lo = hi
+    total["hist"] = {str(k): v for k, v in sorted(total["hist"].items())}
+    doc = {"lo": 4, "hi": N + 1, "p_fast": args.p_fast,
+           "source": "oracle/gb_oracle.c via scripts/make_golden.py (CPU oracle only)",
+           "oracle_seconds": round(t_all, 1), "result": total}
+    with open(outp, "w") as f:
+        json.dump(doc, f, indent=1)
+    print("wrote", outp)
+
+
+if __name__ == "__main__":
+    main()
