@@ -1,0 +1,337 @@
+// gb_api.cu -- the C ABI declared in include/gb.h: argument checking, workspace
+// carve-out, range planning and kernel launches.  No compute happens here; every
+// step of the path runs in the kernels of gb_kernels.cu.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <vector>
+
+#include "gb_internal.h"
+
+using namespace gb;
+
+namespace {
+
+uint64_t isqrt_u64(uint64_t x)
+{
+    uint64_t lo = 0, hi = 4294967296ull;      // lo^2 <= x < hi^2
+    while (hi - lo > 1) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if ((unsigned __int128)mid * mid <= x) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+    uint64_t R, bits_words, list_cap, n_blk;
+    uint64_t off_bits, off_primes, off_magic, off_blk, off_counter, off_res, off_dump, total;
+};
+
+bool plan(uint64_t hi_max, uint32_t p_max, Layout &L)
+{
+    if (hi_max < 5 || hi_max > GB_HI_LIMIT || p_max < 3 || p_max > GB_PMAX_LIMIT) return false;
+    uint64_t R = isqrt_u64(hi_max - 1);
+    R = std::max<uint64_t>(R, p_max);
+    R = std::max<uint64_t>(R, 1024);
+    if (R > 0xFFFFFFFFull - 64) return false;   // primes are u32
+    L.R = R;
+    L.bits_words = ((R - 3) / 2) / 64 + 1;
+    // pi(x) < 1.25506 x / ln x (Rosser-Schoenfeld, x > 1)
+    double bound = 1.25506 * (double)R / __builtin_log((double)R);
+    L.list_cap = (uint64_t)bound + 64;
+    L.n_blk = (L.bits_words + kScanBlockWords - 1) / kScanBlockWords;
+    uint64_t o = 0;
+    L.off_bits = o;    o = align_up(o + 8 * L.bits_words, 256);
+    L.off_primes = o;  o = align_up(o + 4 * L.list_cap, 256);
+    L.off_magic = o;   o = align_up(o + 8 * L.list_cap, 256);
+    L.off_blk = o;     o = align_up(o + 8 * (L.n_blk + 1), 256);
+    L.off_counter = o; o = align_up(o + 256, 256);
+    L.off_res = o;     o = align_up(o + 8 * (uint64_t)GB_RESULT_WORDS, 256);
+    L.off_dump = o;    o = align_up(o + 4 * kDumpScratch, 256);
+    L.total = o;
+    return true;
+}
+
+inline cudaStream_t S(void *s) { return (cudaStream_t)s; }
+
+// count of list entries <= x
+uint32_t count_le(const std::vector<uint32_t> &v, uint64_t x)
+{
+    if (x >= 0xFFFFFFFFull) return (uint32_t)v.size();
+    return (uint32_t)(std::upper_bound(v.begin(), v.end(), (uint32_t)x) - v.begin());
+}
+
+SievePrimes sieve_primes(const gb_ctx *c, uint64_t sqrt_bound)
+{
+    SievePrimes sp;
+    sp.primes = c->primes;
+    sp.magic = c->magic;
+    sp.i_med = count_le(c->h_primes, 31);
+    sp.i_big = count_le(c->h_primes, kWarpPrimeMax);
+    sp.n_use = count_le(c->h_primes, sqrt_bound);
+    return sp;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int d)
+    {
+        cudaGetDevice(&prev);
+        if (prev != d) cudaSetDevice(d);
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char *gb_status_string(gb_status s)
+{
+    switch (s) {
+    case GB_OK: return "GB_OK";
+    case GB_EINVAL: return "GB_EINVAL: invalid argument";
+    case GB_ERANGE: return "GB_ERANGE: range needs base primes beyond the context's hi_max";
+    case GB_EWORKSPACE: return "GB_EWORKSPACE: workspace too small";
+    case GB_ECUDA: return "GB_ECUDA: CUDA error";
+    case GB_EINTERNAL: return "GB_EINTERNAL: internal error";
+    }
+    return "unknown gb_status";
+}
+
+size_t gb_ctx_workspace_bytes(uint64_t hi_max, uint32_t p_max)
+{
+    Layout L;
+    if (!plan(hi_max, p_max, L)) return 0;
+    return (size_t)L.total;
+}
+
+gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_max, uint32_t p_max,
+                        void *d_workspace, size_t ws_bytes, void *stream)
+{
+    if (!out) return GB_EINVAL;
+    *out = nullptr;
+    Layout L;
+    if (!plan(hi_max, p_max, L) || !d_workspace || ((uintptr_t)d_workspace & 255)) return GB_EINVAL;
+    if ((origin & 1) || origin > hi_max || ((hi_max - origin) >> 1) >= (1ull << GB_KEY_SHIFT))
+        return GB_EINVAL;
+    if (ws_bytes < L.total) return GB_EWORKSPACE;
+    DeviceGuard g(device);
+    gb_ctx *c = new (std::nothrow) gb_ctx();
+    if (!c) return GB_EINTERNAL;
+    char *ws = (char *)d_workspace;
+    c->device = device;
+    c->origin = origin;
+    c->hi_max = hi_max;
+    c->p_max = p_max;
+    c->R = L.R;
+    c->bits = (uint64_t *)(ws + L.off_bits);
+    c->bits_words = L.bits_words;
+    c->primes = (uint32_t *)(ws + L.off_primes);
+    c->magic = (uint64_t *)(ws + L.off_magic);
+    c->blk = (uint64_t *)(ws + L.off_blk);
+    c->counter = (uint32_t *)(ws + L.off_counter);
+    c->res_scratch = (int64_t *)(ws + L.off_res);
+    c->dump_scratch = (uint32_t *)(ws + L.off_dump);
+    if (cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+        delete c;
+        return GB_ECUDA;
+    }
+    cudaStream_t st = S(stream);
+    // K-BASE stage 1: seed primes <= isqrt(R) (with per-prime magic)
+    const uint64_t s = isqrt_u64(L.R);
+    if (launch_seed(s, c->primes, c->magic, c->counter, st) != cudaSuccess) { delete c; return GB_ECUDA; }
+    uint32_t n_seed = 0;
+    if (cudaMemcpyAsync(&n_seed, c->counter, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+        delete c;
+        return GB_ECUDA;
+    }
+    c->h_primes.resize(n_seed);
+    if (cudaMemcpy(c->h_primes.data(), c->primes, 4ull * n_seed, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        delete c;
+        return GB_ECUDA;
+    }
+    // K-BASE stage 2: segment sieve of [3, R] with the seeds
+    SegmentArgs sa;
+    sa.sp = sieve_primes(c, s);
+    sa.g_lo = 0;
+    sa.n_words32 = 2 * L.bits_words;
+    sa.o_limit = (L.R - 3) / 2 + 1;            // odd q <= R only
+    sa.out = (uint32_t *)c->bits;
+    if (launch_segment(sa, st) != cudaSuccess) { delete c; return GB_ECUDA; }
+    // K-BASE stage 3: compaction into the ascending list (+ magic)
+    if (launch_count_bits(c->bits, L.bits_words, c->blk, st) != cudaSuccess ||
+        launch_scan(c->blk, L.n_blk, st) != cudaSuccess ||
+        launch_scatter(c->bits, L.bits_words, c->blk, c->primes, c->magic, st) != cudaSuccess) {
+        delete c;
+        return GB_ECUDA;
+    }
+    uint64_t n_base = 0;
+    if (cudaMemcpyAsync(&n_base, c->blk + L.n_blk, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+        delete c;
+        return GB_ECUDA;
+    }
+    if (n_base > L.list_cap) { delete c; return GB_EINTERNAL; }
+    c->n_base = n_base;
+    c->h_primes.resize(n_base);
+    if (cudaMemcpy(c->h_primes.data(), c->primes, 4ull * n_base, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        delete c;
+        return GB_ECUDA;
+    }
+    // verify kernel smem limit for the largest p_max this ctx accepts
+    const uint32_t n_cand = count_le(c->h_primes, p_max);
+    const uint32_t kmax = (c->h_primes[n_cand - 1] - 1) / 2;
+    const size_t smem_max = 4ull * ((kmax >> 5) + 1 + kTileWords);
+    if (configure_verify(smem_max) != cudaSuccess) { delete c; return GB_ECUDA; }
+    *out = c;
+    return GB_OK;
+}
+
+void gb_ctx_destroy(gb_ctx *ctx) { delete ctx; }
+
+gb_status gb_ctx_info(const gb_ctx *ctx, uint64_t *n_base_primes, uint64_t *R)
+{
+    if (!ctx) return GB_EINVAL;
+    if (n_base_primes) *n_base_primes = ctx->n_base;
+    if (R) *R = ctx->R;
+    return GB_OK;
+}
+
+gb_status gb_ctx_tables(const gb_ctx *ctx, const uint64_t **d_bits, const uint32_t **d_primes)
+{
+    if (!ctx) return GB_EINVAL;
+    if (d_bits) *d_bits = ctx->bits;
+    if (d_primes) *d_primes = ctx->primes;
+    return GB_OK;
+}
+
+gb_status gb_sieve_segment(gb_ctx *ctx, uint64_t word_lo, uint64_t n_words, uint64_t *d_words,
+                           void *stream)
+{
+    if (!ctx || ((uintptr_t)d_words & 7)) return GB_EINVAL;
+    if (n_words == 0) return GB_OK;
+    if (!d_words || word_lo > (1ull << 58) || n_words > (1ull << 58)) return GB_EINVAL;
+    const uint64_t top_o = 64 * (word_lo + n_words) - 1;   // largest odd index
+    if (top_o > (GB_HI_LIMIT - 3) / 2) return GB_EINVAL;
+    const uint64_t q_max = 3 + 2 * top_o;
+    const uint64_t r = isqrt_u64(q_max);
+    if (r > ctx->R) return GB_ERANGE;
+    DeviceGuard g(ctx->device);
+    SegmentArgs sa;
+    sa.sp = sieve_primes(ctx, r);
+    sa.g_lo = 2 * word_lo;
+    sa.n_words32 = 2 * n_words;
+    sa.o_limit = UINT64_MAX;
+    sa.out = (uint32_t *)d_words;
+    return launch_segment(sa, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
+}
+
+gb_status gb_result_init(int64_t *d_result, void *stream)
+{
+    if (!d_result || ((uintptr_t)d_result & 7)) return GB_EINVAL;
+    return launch_result_init(d_result, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
+}
+
+gb_status gb_result_finalize(int64_t *d_result, void *stream)
+{
+    if (!d_result || ((uintptr_t)d_result & 7)) return GB_EINVAL;
+    return launch_result_finalize(d_result, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
+}
+
+gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_max,
+                             uint64_t fallback_p_cap, int64_t *d_result, uint32_t *d_pmin_dump,
+                             void *stream)
+{
+    if (!ctx || !d_result || ((uintptr_t)d_result & 7) || ((uintptr_t)d_pmin_dump & 3))
+        return GB_EINVAL;
+    if (lo > hi || hi > GB_HI_LIMIT || p_max < 3 || p_max > ctx->p_max) return GB_EINVAL;
+    const uint64_t lo_e = lo < 4 ? 4 : lo + (lo & 1);
+    if (hi <= lo_e) return GB_OK;                            // empty range: no launch
+    if (hi > ctx->hi_max) return GB_ERANGE;
+    if (lo_e < ctx->origin || ((hi - ctx->origin) >> 1) >= (1ull << GB_KEY_SHIFT)) return GB_EINVAL;
+    const uint64_t n_last = (hi - 1) & ~1ull;                // largest even n < hi
+    VerifyArgs a;
+    a.e_lo = (lo_e - 4) / 2;
+    a.e_hi = (n_last - 4) / 2 + 1;
+    const uint64_t r = isqrt_u64(hi - 1);
+    if (r > ctx->R) return GB_ERANGE;
+    a.sp = sieve_primes(ctx, r);
+    a.n_cand = count_le(ctx->h_primes, p_max);
+    if (a.n_cand == 0) return GB_EINVAL;
+    const uint32_t p_top = ctx->h_primes[a.n_cand - 1];
+    a.halo = (((p_top - 1) / 2) >> 5) + 1;
+    a.u_first = a.e_lo >> 5;
+    a.u_end = ((a.e_hi - 1) >> 5) + 1;
+    a.n_tiles = (a.u_end - a.u_first + kTileWords - 1) / kTileWords;
+    a.origin = ctx->origin;
+    a.p_fallback = (uint64_t)p_top + 2;
+    a.cap = fallback_p_cap;
+    a.base_bits = ctx->bits;
+    a.R = ctx->R;
+    a.n_base = (uint32_t)ctx->n_base;
+    a.result = d_result;
+    a.dump = d_pmin_dump;
+    DeviceGuard g(ctx->device);
+    const size_t smem = 4ull * (a.halo + kTileWords);
+    const int per_sm = verify_blocks_per_sm(smem);
+    const uint64_t max_grid = (uint64_t)per_sm * ctx->num_sms;
+    const int grid = (int)std::min<uint64_t>(a.n_tiles, max_grid);
+    return launch_verify(a, grid, smem, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
+}
+
+gb_status gb_verify_range(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_max, int64_t *d_result,
+                          uint32_t *d_pmin_dump, void *stream)
+{
+    return gb_verify_range_ex(ctx, lo, hi, p_max, UINT64_MAX, d_result, d_pmin_dump, stream);
+}
+
+gb_status gb_verify_range_host(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_max,
+                               int64_t *h_result, uint32_t *h_pmin_dump, void *stream)
+{
+    if (!ctx || !h_result) return GB_EINVAL;
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = S(stream);
+    gb_status s = gb_result_init(ctx->res_scratch, stream);
+    if (s != GB_OK) return s;
+    const uint64_t lo_e = lo < 4 ? 4 : lo + (lo & 1);
+    if (!h_pmin_dump) {
+        s = gb_verify_range(ctx, lo, hi, p_max, ctx->res_scratch, nullptr, stream);
+        if (s != GB_OK) return s;
+    } else {
+        // chunks of kDumpScratch evens through the device scratch
+        for (uint64_t c = lo_e; c < hi; c += 2 * kDumpScratch) {
+            const uint64_t ce = std::min<uint64_t>(hi, c + 2 * kDumpScratch);
+            s = gb_verify_range(ctx, c, ce, p_max, ctx->res_scratch, ctx->dump_scratch, stream);
+            if (s != GB_OK) return s;
+            const uint64_t cnt = (ce - c + 1) / 2;
+            if (cudaMemcpyAsync(h_pmin_dump + (c - lo_e) / 2, ctx->dump_scratch, 4 * cnt,
+                                cudaMemcpyDeviceToHost, st) != cudaSuccess)
+                return GB_ECUDA;
+        }
+    }
+    s = gb_result_finalize(ctx->res_scratch, stream);
+    if (s != GB_OK) return s;
+    if (cudaMemcpyAsync(h_result, ctx->res_scratch, 8ull * GB_RESULT_WORDS, cudaMemcpyDeviceToHost,
+                        st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return GB_ECUDA;
+    return GB_OK;
+}
+
+gb_status gb_is_prime_u64(const uint64_t *d_x, uint8_t *d_out, uint64_t n, void *stream)
+{
+    if (n && (!d_x || !d_out || ((uintptr_t)d_x & 7))) return GB_EINVAL;
+    return launch_is_prime(d_x, d_out, n, nullptr, 0, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
+}
+
+}  // extern "C"

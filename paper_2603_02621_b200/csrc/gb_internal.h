@@ -1,0 +1,96 @@
+// gb_internal.h -- shared between the C-ABI layer (gb_api.cu) and the kernels
+// (gb_kernels.cu).  Product code only; nothing here is visible to oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "gb.h"
+
+namespace gb {
+
+// ---- tiling constants (tuned for sm_100a: 148 SMs, 228 KB smem / SM) ----
+constexpr int kThreads = 512;              // threads per CTA, every kernel
+constexpr int kTileWords = 16384;          // 32-bit U words per verify tile = 524288 evens
+constexpr int kSieveTileWords = 16384;     // 32-bit words per gb_sieve_segment CTA
+constexpr int kHistSmem = 1024;            // histogram bins kept in shared memory
+constexpr uint32_t kWarpPrimeMax = 8192;   // primes <= this: one warp per prime
+constexpr int kTinyPrimes = 10;            // 3..31 sieved by word patterns
+constexpr uint64_t kDumpScratch = 1ull << 24;  // u32 entries of host-API dump scratch
+constexpr int kScanBlockWords = 2048;      // u64 words per K-BASE compaction block
+
+// Arguments of the window sieve (K-SIEVE) shared by every caller.
+struct SievePrimes {
+    const uint32_t *primes;   // odd primes ascending (3, 5, 7, ...)
+    const uint64_t *magic;    // floor((2^64-1)/p) per prime
+    uint32_t i_med;           // first index with p > 31 (word patterns below)
+    uint32_t i_big;           // first index with p > kWarpPrimeMax
+    uint32_t n_use;           // primes usable (p^2 beyond the window are skipped)
+};
+
+struct SegmentArgs {
+    SievePrimes sp;
+    uint64_t g_lo;            // first 32-bit word (o-space) of the output
+    uint64_t n_words32;       // 32-bit words to produce
+    uint64_t o_limit;         // bits with o >= o_limit are cleared (UINT64_MAX: none)
+    uint32_t *out;            // n_words32 words
+};
+
+struct VerifyArgs {
+    SievePrimes sp;
+    uint32_t n_cand;          // odd primes p <= p_max used by the fast path
+    uint32_t halo;            // H32 = ((p_cand_max-1)/2 >> 5) + 1 words below a tile
+    uint64_t e_lo, e_hi;      // even-index range [e_lo, e_hi), e(n) = (n-4)/2
+    uint64_t u_first;         // first 32-bit U word
+    uint64_t u_end;           // one past the last U word
+    uint64_t n_tiles;
+    uint64_t origin;          // MAX_KEY origin
+    uint64_t p_fallback;      // first odd candidate after the fast path (p_cand_max + 2)
+    uint64_t cap;             // fallback p cap (test hook)
+    const uint64_t *base_bits;  // resident odd bitset of [3, R]
+    uint64_t R;
+    uint32_t n_base;          // odd primes in the resident list
+    int64_t *result;
+    uint32_t *dump;           // nullable
+};
+
+// Launchers (gb_kernels.cu).  Each returns the cudaGetLastError() of its launch.
+cudaError_t launch_seed(uint64_t s, uint32_t *primes, uint64_t *magic, uint32_t *d_count,
+                        cudaStream_t st);
+cudaError_t launch_segment(const SegmentArgs &a, cudaStream_t st);
+cudaError_t launch_count_bits(const uint64_t *bits, uint64_t n_words, uint64_t *blk,
+                              cudaStream_t st);
+cudaError_t launch_scan(uint64_t *blk, uint64_t n_blk, cudaStream_t st);
+cudaError_t launch_scatter(const uint64_t *bits, uint64_t n_words, const uint64_t *blk,
+                           uint32_t *primes, uint64_t *magic, cudaStream_t st);
+cudaError_t launch_result_init(int64_t *res, cudaStream_t st);
+cudaError_t launch_result_finalize(int64_t *res, cudaStream_t st);
+cudaError_t launch_verify(const VerifyArgs &a, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_is_prime(const uint64_t *x, uint8_t *out, uint64_t n, const uint64_t *bits,
+                            uint64_t R, cudaStream_t st);
+cudaError_t configure_verify(size_t smem_max);
+int verify_blocks_per_sm(size_t smem);
+
+void count_launch();
+
+}  // namespace gb
+
+struct gb_ctx {
+    int device;
+    int num_sms;
+    uint64_t origin, hi_max, R;
+    uint32_t p_max;
+    cudaStream_t create_stream;
+    // workspace carve-out
+    uint64_t *bits;        // odd bitset [3, R]
+    uint64_t bits_words;
+    uint32_t *primes;      // odd primes <= R
+    uint64_t *magic;
+    uint64_t *blk;         // K-BASE scratch
+    uint32_t *counter;     // K-BASE scratch
+    int64_t *res_scratch;  // host API result
+    uint32_t *dump_scratch;
+    uint64_t n_base;
+    std::vector<uint32_t> h_primes;  // host copy for range planning
+};

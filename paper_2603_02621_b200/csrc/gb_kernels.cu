@@ -1,0 +1,596 @@
+// gb_kernels.cu -- sm_100a kernels of the segmented double-sieve Goldbach verifier.
+//
+//   K-BASE   : seed sieve + segment sieve + compaction of the resident small-prime
+//              table ("permanently resident small-primes bitset").
+//   K-SIEVE  : odd-only bit-packed window sieve in shared memory (PAPER.md:76-78,
+//              moved from the host CPU to the GPU as PAPER.md:421 proposes).
+//   K-VERIFY : K-SIEVE fused with the inverted bulk-marking loop (PAPER.md:73-76,
+//              406-410) and the on-GPU exhaustive fallback.
+//
+// Bit layouts: odd q <-> o(q) = (q-3)/2, even n <-> e(n) = (n-4)/2,
+// both packed 32 bits per word here (a 64-bit word of the paper's layout is two
+// consecutive 32-bit words, little-endian).  For odd p = 2k+1, o(n-p) = e(n) - k,
+// so "n - p is prime" over a U word is the O bitset shifted up by k bits.
+#include <stdint.h>
+
+#include <atomic>
+
+#include "gb_internal.h"
+#include "mr64.cuh"
+
+namespace gb {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace gb
+
+extern "C" uint64_t gb_launch_count(void) { return gb::g_launches.load(); }
+
+namespace gb {
+
+constexpr uint32_t FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t mod_magic(uint64_t x, uint32_t p, uint64_t m)
+{
+    // x mod p with m = floor((2^64-1)/p): the quotient estimate is low by <= 2.
+    uint64_t q = __umul64hi(x, m);
+    uint64_t r = x - q * p;
+    while (r >= p) r -= p;
+    return (uint32_t)r;
+}
+
+// first local bit (relative to o_lo) of an odd multiple of p that is >= p^2 and
+// >= o_lo, i.e. o = (p*m - 3)/2 with m odd; in o-space the multiples of p are the
+// residue class o == (p-3)/2 (mod p).  Returns UINT64_MAX if p^2 is beyond o_hi.
+__device__ __forceinline__ uint64_t first_hit(uint32_t p, uint64_t magic, int64_t o_lo, int64_t o_hi)
+{
+    const int64_t opp = (int64_t)(((uint64_t)p * p - 3) >> 1);
+    if (opp >= o_hi) return UINT64_MAX;
+    const uint64_t ostart = (uint64_t)(opp > o_lo ? opp : o_lo);
+    const uint32_t r = mod_magic(ostart, p, magic);
+    const uint32_t rp = (p - 3) >> 1;
+    const uint32_t delta = rp >= r ? rp - r : rp + p - r;
+    return ostart + delta - (uint64_t)o_lo;
+}
+
+// bits 0, P, 2P, ... < 32
+__host__ __device__ constexpr uint32_t tiny_pattern(int P, int i = 0)
+{
+    return i >= 32 ? 0u : ((1u << i) | tiny_pattern(P, i + P));
+}
+template <int P>
+struct Tiny {
+    static constexpr uint32_t value = tiny_pattern(P);
+};
+
+// ---------------------------------------------------------------------------
+// K-SIEVE: window of nw 32-bit words, word i <-> o in [32(g0+i), 32(g0+i)+32).
+// Words with g0 + i < 0 (q <= 1) are zero.  Bit = 1 iff q = 3 + 2o is prime, for
+// every q whose square root is covered by sp (callers guarantee it).
+// Ends WITHOUT a barrier; callers __syncthreads() before reading `win`.
+// ---------------------------------------------------------------------------
+__device__ void sieve_window(uint32_t *win, int64_t g0, uint32_t nw, const SievePrimes &sp)
+{
+    const int tid = threadIdx.x, nt = blockDim.x;
+    // Phase T: primes 3..31 by shifted word patterns.  For word g the first
+    // multiple sits at bit s_p = ((p-3)/2 - 32 g) mod p; mask = pattern_p << s_p.
+    {
+        // per-thread phases, advanced incrementally by 32*nt words
+        int64_t g = g0 + tid;
+        uint64_t gg = g < 0 ? 0 : (uint64_t)g;
+#define GB_PHASE(P) int s##P = (int)(((uint64_t)(P - 3) / 2 + (uint64_t)P * 32 - (32 * (gg % P)) % P) % P); \
+                    const int d##P = (32 * nt) % P;
+        GB_PHASE(3) GB_PHASE(5) GB_PHASE(7) GB_PHASE(11) GB_PHASE(13)
+        GB_PHASE(17) GB_PHASE(19) GB_PHASE(23) GB_PHASE(29) GB_PHASE(31)
+#undef GB_PHASE
+        for (int64_t i = tid; i < (int64_t)nw; i += nt, g += nt) {
+            uint32_t w = 0;
+            if (g >= 0) {
+                uint32_t c = (Tiny<3>::value << s3) | (Tiny<5>::value << s5) |
+                             (Tiny<7>::value << s7) | (Tiny<11>::value << s11) |
+                             (Tiny<13>::value << s13) | (Tiny<17>::value << s17) |
+                             (Tiny<19>::value << s19) | (Tiny<23>::value << s23) |
+                             (Tiny<29>::value << s29) | (Tiny<31>::value << s31);
+                w = ~c;
+                if (g == 0) w |= 0x65B7u;   // restore 3,5,7,11,13,17,19,23,29,31 (o = 0,1,2,4,5,7,8,10,13,14)
+            }
+            win[i] = w;
+            if (g >= 0) {
+#define GB_ADV(P) s##P -= d##P; if (s##P < 0) s##P += P;
+                GB_ADV(3) GB_ADV(5) GB_ADV(7) GB_ADV(11) GB_ADV(13)
+                GB_ADV(17) GB_ADV(19) GB_ADV(23) GB_ADV(29) GB_ADV(31)
+#undef GB_ADV
+            } else if (g + nt >= 0) {
+                // crossing from negative to non-negative words: recompute phases at g + nt
+                uint64_t g2 = (uint64_t)(g + nt);
+#define GB_RE(P) s##P = (int)(((uint64_t)(P - 3) / 2 + (uint64_t)P * 32 - (32 * (g2 % P)) % P) % P);
+                GB_RE(3) GB_RE(5) GB_RE(7) GB_RE(11) GB_RE(13)
+                GB_RE(17) GB_RE(19) GB_RE(23) GB_RE(29) GB_RE(31)
+#undef GB_RE
+            }
+        }
+    }
+    __syncthreads();
+    const int64_t o_lo = g0 * 32;
+    const int64_t o_hi = (g0 + (int64_t)nw) * 32;
+    const uint32_t nbits = nw * 32;
+    const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+    // Phase M: medium primes (31 < p <= kWarpPrimeMax), one warp per prime.
+    const uint32_t m_end = sp.i_big < sp.n_use ? sp.i_big : sp.n_use;
+    for (uint32_t pi = sp.i_med + warp; pi < m_end; pi += nwarps) {
+        const uint32_t p = __ldg(sp.primes + pi);
+        const uint64_t off = first_hit(p, __ldg(sp.magic + pi), o_lo, o_hi);
+        if (off == UINT64_MAX) break;
+        for (uint64_t b = off + (uint64_t)lane * p; b < nbits; b += 32ull * p)
+            atomicAnd(win + (b >> 5), ~(1u << (b & 31)));
+    }
+    // Phase B: large primes, one thread per prime.
+    const uint32_t b_begin = sp.i_big > sp.i_med ? sp.i_big : sp.i_med;
+    for (uint32_t pi = b_begin + tid; pi < sp.n_use; pi += nt) {
+        const uint32_t p = __ldg(sp.primes + pi);
+        const uint64_t off = first_hit(p, __ldg(sp.magic + pi), o_lo, o_hi);
+        if (off == UINT64_MAX) break;
+        for (uint64_t b = off; b < nbits; b += p)
+            atomicAnd(win + (b >> 5), ~(1u << (b & 31)));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// gb_sieve_segment / K-BASE stage 2
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) segment_kernel(SegmentArgs a)
+{
+    extern __shared__ uint32_t win[];          // kSieveTileWords words
+    const uint64_t t0 = (uint64_t)blockIdx.x * kSieveTileWords;
+    const uint32_t nw = (uint32_t)min((uint64_t)kSieveTileWords, a.n_words32 - t0);
+    const int64_t g0 = (int64_t)(a.g_lo + t0);
+    sieve_window(win, g0, nw, a.sp);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) {
+        uint32_t w = win[i];
+        const uint64_t o0 = (uint64_t)(g0 + i) * 32;
+        if (o0 + 32 > a.o_limit) {
+            w = o0 >= a.o_limit ? 0u : (w & ((1u << (a.o_limit - o0)) - 1u));
+        }
+        a.out[t0 + i] = w;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K-BASE stage 1: primes <= s (s <= 65535) in one CTA, byte sieve in smem.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) seed_kernel(uint32_t s, uint32_t *primes, uint64_t *magic,
+                                                    uint32_t *d_count)
+{
+    extern __shared__ uint8_t flag[];
+    for (uint32_t i = threadIdx.x; i <= s; i += blockDim.x) flag[i] = (i >= 2);
+    __syncthreads();
+    for (uint32_t i = 2; i * i <= s; ++i) {
+        __syncthreads();
+        if (!flag[i]) continue;   // uniform: flag[i] is final once all i' < i are done
+        for (uint32_t m = i * i + threadIdx.x * i; m <= s; m += blockDim.x * i) flag[m] = 0;
+    }
+    __syncthreads();
+    __shared__ uint32_t cnt;
+    if (threadIdx.x == 0) {
+        uint32_t c = 0;
+        for (uint32_t i = 3; i <= s; i += 2)
+            if (flag[i]) primes[c++] = i;
+        cnt = c;
+        *d_count = c;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) magic[i] = ~0ull / primes[i];
+}
+
+// ---------------------------------------------------------------------------
+// K-BASE stage 3: compaction of the bitset into the ascending prime list.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) count_bits_kernel(const uint64_t *bits, uint64_t n_words,
+                                                         uint64_t *blk)
+{
+    const uint64_t w0 = (uint64_t)blockIdx.x * kScanBlockWords;
+    uint32_t c = 0;
+    for (uint64_t i = w0 + threadIdx.x; i < w0 + kScanBlockWords && i < n_words; i += blockDim.x)
+        c += __popcll(bits[i]);
+    c = __reduce_add_sync(FULL, c);
+    __shared__ uint32_t ws[8];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t t = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += ws[i];
+        blk[blockIdx.x] = t;
+    }
+}
+
+// exclusive scan of blk[0..n) in place; blk[n] = total.  One CTA.
+__global__ void __launch_bounds__(1024) scan_kernel(uint64_t *blk, uint64_t n)
+{
+    __shared__ uint64_t part[1024];
+    const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
+    const uint64_t b = threadIdx.x * per, e = min(n, b + per);
+    uint64_t s = 0;
+    for (uint64_t i = b; i < e; ++i) s += blk[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t run = 0;
+        for (int i = 0; i < (int)blockDim.x; ++i) { uint64_t v = part[i]; part[i] = run; run += v; }
+        blk[n] = run;
+    }
+    __syncthreads();
+    uint64_t run = part[threadIdx.x];
+    for (uint64_t i = b; i < e; ++i) { uint64_t v = blk[i]; blk[i] = run; run += v; }
+}
+
+__global__ void __launch_bounds__(256) scatter_kernel(const uint64_t *bits, uint64_t n_words,
+                                                      const uint64_t *blk, uint32_t *primes,
+                                                      uint64_t *magic)
+{
+    // each thread owns kScanBlockWords/256 = 8 consecutive words of this block
+    constexpr int per = kScanBlockWords / 256;
+    const uint64_t w0 = (uint64_t)blockIdx.x * kScanBlockWords + (uint64_t)threadIdx.x * per;
+    uint32_t c = 0;
+    for (int i = 0; i < per; ++i)
+        if (w0 + i < n_words) c += __popcll(bits[w0 + i]);
+    // block-exclusive scan of c
+    __shared__ uint32_t sc[256];
+    sc[threadIdx.x] = c;
+    __syncthreads();
+    for (int off = 1; off < 256; off <<= 1) {
+        uint32_t v = threadIdx.x >= (unsigned)off ? sc[threadIdx.x - off] : 0;
+        __syncthreads();
+        sc[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint64_t idx = blk[blockIdx.x] + sc[threadIdx.x] - c;
+    for (int i = 0; i < per; ++i) {
+        const uint64_t w = w0 + i;
+        if (w >= n_words) break;
+        uint64_t x = bits[w];
+        while (x) {
+            const int b = __ffsll((long long)x) - 1;
+            x &= x - 1;
+            const uint64_t q = 3 + 2 * (64 * w + (uint64_t)b);
+            primes[idx] = (uint32_t)q;
+            magic[idx] = ~0ull / q;
+            ++idx;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// result vector
+// ---------------------------------------------------------------------------
+__global__ void result_init_kernel(int64_t *r)
+{
+    for (int i = threadIdx.x; i < GB_RESULT_WORDS; i += blockDim.x) r[i] = 0;
+    if (threadIdx.x == 0) {
+        r[GB_R_VERSION] = GB_RESULT_VERSION;
+        r[GB_R_FIRST_UNRESOLVED_N] = INT64_MAX;
+    }
+}
+
+__global__ void result_finalize_kernel(int64_t *r)
+{
+    const uint64_t c = (uint64_t)r[GB_R_CHK_RAW];
+    r[GB_R_CHK_LO32] += (int64_t)(c & 0xffffffffu);
+    r[GB_R_CHK_HI32] += (int64_t)(c >> 32);
+    r[GB_R_CHK_RAW] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// fallback (subsystem (d)): warp-cooperative exhaustive scan for one n.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool is_prime_dev(uint64_t x, const uint64_t *bits, uint64_t R)
+{
+    if (x < 3) return x == 2;
+    if ((x & 1) == 0) return false;
+    if (x <= R) {
+        const uint64_t o = (x - 3) >> 1;
+        return (__ldg(bits + (o >> 6)) >> (o & 63)) & 1;
+    }
+    return mr64_odd(x);
+}
+
+// Minimal prime p in [p_start, min(n/2, cap)] (p_start odd) with n - p prime, or 0.
+// All 32 lanes call it with the same n; lane l tests p_start + 2l + 64i.
+__device__ uint64_t fallback_scan(uint64_t n, uint64_t p_start, uint64_t cap,
+                                  const uint64_t *bits, uint64_t R)
+{
+    const int lane = threadIdx.x & 31;
+    const uint64_t half = n / 2;
+    const uint64_t lim = half < cap ? half : cap;
+    for (uint64_t base = p_start; base <= lim; base += 64) {
+        const uint64_t p = base + 2 * (uint64_t)lane;
+        bool ok = false;
+        if (p <= lim) ok = is_prime_dev(p, bits, R) && is_prime_dev(n - p, bits, R);
+        const uint32_t m = __ballot_sync(FULL, ok);
+        if (m) return __shfl_sync(FULL, p, __ffs(m) - 1);
+    }
+    return 0;
+}
+
+// histogram bin of an odd prime p found by the fallback: 1 + #primes <= p
+__device__ uint32_t bin_of_prime(uint64_t p, const uint32_t *primes, uint32_t n_base)
+{
+    if (p > 65521) return GB_NBINS - 1;
+    uint32_t lo = 0, hi = n_base;           // first index with primes[i] >= p
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(primes + mid) < p) lo = mid + 1; else hi = mid;
+    }
+    return lo + 2;                           // primes[0] = 3 is bin 2
+}
+
+// ---------------------------------------------------------------------------
+// K-VERIFY: fused sieve -> inverted bulk marking -> fallback, persistent CTAs.
+// ---------------------------------------------------------------------------
+struct Acc {
+    uint64_t evens = 0, verified = 0, fast_unres = 0, unres = 0, sum = 0, chk = 0;
+    uint64_t key = 0, first_unres = UINT64_MAX;
+};
+
+__device__ __forceinline__ uint64_t make_key(uint64_t p, uint64_t n, uint64_t origin)
+{
+    const uint64_t pk = p < (1ull << 23) ? p : (1ull << 23) - 1;
+    const uint64_t idx = (n - origin) >> 1;
+    return (pk << GB_KEY_SHIFT) | ((1ull << GB_KEY_SHIFT) - 1 - idx);
+}
+
+__device__ __forceinline__ void hist_add(uint32_t *sh_hist, int64_t *res, uint32_t bin, uint32_t c)
+{
+    if (bin >= GB_NBINS) bin = GB_NBINS - 1;
+    if (bin < (uint32_t)kHistSmem) atomicAdd(sh_hist + bin, c);
+    else atomicAdd((unsigned long long *)(res + GB_R_HIST + bin), (unsigned long long)c);
+}
+
+template <bool DUMP>
+__global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
+{
+    extern __shared__ uint32_t win[];          // halo + kTileWords words
+    __shared__ uint32_t sh_hist[kHistSmem];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    for (int i = tid; i < kHistSmem; i += blockDim.x) sh_hist[i] = 0;
+    Acc acc;
+    const uint64_t e_dump0 = a.e_lo;
+
+    for (uint64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+        const uint64_t u0 = a.u_first + tile * kTileWords;
+        const uint32_t tw = (uint32_t)min((uint64_t)kTileWords, a.u_end - u0);
+        __syncthreads();                      // previous tile fully consumed
+        sieve_window(win, (int64_t)u0 - a.halo, a.halo + tw, a.sp);
+        __syncthreads();
+
+        // rounds of 32 words, one word per lane, interleaved over warps
+        const uint32_t n_rounds = (tw + 31) >> 5;
+        for (uint32_t r = warp; r < n_rounds; r += nwarps) {
+            const uint32_t li = r * 32 + lane;
+            const uint64_t u = u0 + li;
+            uint32_t U = 0;
+            if (li < tw) {
+                const uint64_t eb = u * 32;
+                U = FULL;
+                if (eb < a.e_lo) U = (a.e_lo - eb >= 32) ? 0u : (U << (a.e_lo - eb));
+                if (eb + 32 > a.e_hi) U &= (a.e_hi <= eb) ? 0u : (FULL >> (eb + 32 - a.e_hi));
+            }
+            acc.evens += __popc(U);
+            uint64_t word_sum = 0;
+            uint32_t lastp = 0, lastb = 0;
+            if (U & 1u && u == 0) {           // n = 4: p_min = 2, the only even p (R2)
+                U &= ~1u;
+                word_sum += 2;
+                acc.verified += 1;
+                lastp = 2; lastb = 1;
+                atomicAdd(sh_hist + 1, 1u);
+                if (DUMP) a.dump[0 - e_dump0] = 2;
+            }
+            const uint32_t base = a.halo + (li < tw ? li : tw - 1);
+            // inverted loop: odd primes ascending; S = O shifted up by k = (p-1)/2
+            for (uint32_t j = 0; j < a.n_cand; ++j) {
+                if (!__any_sync(FULL, U != 0)) break;
+                const uint32_t p = __ldg(a.sp.primes + j);
+                const uint32_t k = p >> 1;
+                const uint32_t wa = k >> 5, bb = k & 31;
+                const uint32_t S = __funnelshift_l(win[base - wa - 1], win[base - wa], bb);
+                const uint32_t nw = U & S;
+                const uint32_t c = __popc(nw);
+                if (nw) {
+                    U ^= nw;
+                    word_sum += (uint64_t)c * p;
+                    acc.verified += c;
+                    lastp = p; lastb = nw;
+                    if (DUMP) {
+                        uint32_t x = nw;
+                        while (x) {
+                            const int b = __ffs(x) - 1;
+                            x &= x - 1;
+                            a.dump[u * 32 + b - e_dump0] = p;
+                        }
+                    }
+                }
+                const uint32_t tot = __reduce_add_sync(FULL, c);
+                if (lane == 0 && tot) hist_add(sh_hist, a.result, j + 2, tot);
+            }
+            if (lastp) {
+                const uint64_t n = 4 + 2 * (u * 32 + (uint64_t)(__ffs(lastb) - 1));
+                const uint64_t key = make_key(lastp, n, a.origin);
+                if (key > acc.key) acc.key = key;
+            }
+            // exhaustive fallback for whatever the fast path left (rare)
+            acc.fast_unres += __popc(U);
+            while (true) {
+                const uint32_t m = __ballot_sync(FULL, U != 0);
+                if (!m) break;
+                const int L = __ffs(m) - 1;
+                const uint32_t lw = __shfl_sync(FULL, U, L);
+                const uint64_t uL = __shfl_sync(FULL, u, L);
+                const int bit = __ffs(lw) - 1;
+                const uint64_t n = 4 + 2 * (uL * 32 + (uint64_t)bit);
+                const uint64_t p = fallback_scan(n, a.p_fallback, a.cap, a.base_bits, a.R);
+                if (lane == L) {
+                    U &= ~(1u << bit);
+                    if (p) {
+                        word_sum += p;
+                        acc.verified += 1;
+                        hist_add(sh_hist, a.result, bin_of_prime(p, a.sp.primes, a.n_base), 1);
+                        const uint64_t key = make_key(p, n, a.origin);
+                        if (key > acc.key) acc.key = key;
+                    } else {
+                        acc.unres += 1;
+                        hist_add(sh_hist, a.result, 0, 1);
+                        if (n < acc.first_unres) acc.first_unres = n;
+                    }
+                    if (DUMP) a.dump[uL * 32 + bit - e_dump0] = (uint32_t)p;
+                }
+            }
+            acc.sum += word_sum;
+            acc.chk += word_sum * u;          // sum p_min * floor((n-4)/64): u = e >> 5
+        }
+    }
+
+    // flush: warp-reduce then one atomic per warp per field
+    __syncthreads();
+    auto wsum = [&](uint64_t v) {
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        return v;
+    };
+    auto wmax = [&](uint64_t v) {
+        for (int o = 16; o; o >>= 1) { uint64_t w = __shfl_xor_sync(FULL, v, o); v = w > v ? w : v; }
+        return v;
+    };
+    auto wmin = [&](uint64_t v) {
+        for (int o = 16; o; o >>= 1) { uint64_t w = __shfl_xor_sync(FULL, v, o); v = w < v ? w : v; }
+        return v;
+    };
+    const uint64_t ev = wsum(acc.evens), vf = wsum(acc.verified), fu = wsum(acc.fast_unres);
+    const uint64_t un = wsum(acc.unres), sm = wsum(acc.sum), ck = wsum(acc.chk);
+    const uint64_t ky = wmax(acc.key), fr = wmin(acc.first_unres);
+    unsigned long long *R = (unsigned long long *)a.result;
+    if (lane == 0) {
+        if (ev) atomicAdd(R + GB_R_EVENS, ev);
+        if (vf) atomicAdd(R + GB_R_VERIFIED, vf);
+        if (fu) atomicAdd(R + GB_R_FASTPATH_UNRESOLVED, fu);
+        if (un) atomicAdd(R + GB_R_UNRESOLVED, un);
+        if (sm) atomicAdd(R + GB_R_SUM_PMIN, sm);
+        if (ck) atomicAdd(R + GB_R_CHK_RAW, ck);
+        if (ky) atomicMax(R + GB_R_MAX_KEY, ky);
+        if (fr != UINT64_MAX) atomicMin(R + GB_R_FIRST_UNRESOLVED_N, fr);
+    }
+    (void)warp;
+    for (int i = tid; i < kHistSmem; i += blockDim.x)
+        if (sh_hist[i]) atomicAdd(R + GB_R_HIST + i, (unsigned long long)sh_hist[i]);
+}
+
+__global__ void is_prime_kernel(const uint64_t *x, uint8_t *out, uint64_t n)
+{
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = is_prime_u64(x[i]) ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+cudaError_t launch_seed(uint64_t s, uint32_t *primes, uint64_t *magic, uint32_t *d_count,
+                        cudaStream_t st)
+{
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 16);
+    if (attr != cudaSuccess) return attr;
+    seed_kernel<<<1, 1024, (size_t)s + 1, st>>>((uint32_t)s, primes, magic, d_count);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_segment(const SegmentArgs &a, cudaStream_t st)
+{
+    const uint64_t nb = (a.n_words32 + kSieveTileWords - 1) / kSieveTileWords;
+    if (nb == 0) return cudaSuccess;
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        segment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSieveTileWords * 4);
+    if (attr != cudaSuccess) return attr;
+    segment_kernel<<<(unsigned)nb, kThreads, kSieveTileWords * 4, st>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_count_bits(const uint64_t *bits, uint64_t n_words, uint64_t *blk, cudaStream_t st)
+{
+    const uint64_t nb = (n_words + kScanBlockWords - 1) / kScanBlockWords;
+    count_bits_kernel<<<(unsigned)nb, 256, 0, st>>>(bits, n_words, blk);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scan(uint64_t *blk, uint64_t n_blk, cudaStream_t st)
+{
+    scan_kernel<<<1, 1024, 0, st>>>(blk, n_blk);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(const uint64_t *bits, uint64_t n_words, const uint64_t *blk,
+                           uint32_t *primes, uint64_t *magic, cudaStream_t st)
+{
+    const uint64_t nb = (n_words + kScanBlockWords - 1) / kScanBlockWords;
+    scatter_kernel<<<(unsigned)nb, 256, 0, st>>>(bits, n_words, blk, primes, magic);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_result_init(int64_t *res, cudaStream_t st)
+{
+    result_init_kernel<<<1, 256, 0, st>>>(res);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_result_finalize(int64_t *res, cudaStream_t st)
+{
+    result_finalize_kernel<<<1, 1, 0, st>>>(res);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t configure_verify(size_t smem_max)
+{
+    cudaError_t e = cudaFuncSetAttribute(verify_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(verify_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem_max);
+}
+
+int verify_blocks_per_sm(size_t smem)
+{
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, verify_kernel<false>, kThreads, smem) !=
+        cudaSuccess)
+        return 1;
+    return nb < 1 ? 1 : nb;
+}
+
+cudaError_t launch_verify(const VerifyArgs &a, int grid, size_t smem, cudaStream_t st)
+{
+    if (a.dump)
+        verify_kernel<true><<<grid, kThreads, smem, st>>>(a);
+    else
+        verify_kernel<false><<<grid, kThreads, smem, st>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_is_prime(const uint64_t *x, uint8_t *out, uint64_t n, const uint64_t *,
+                            uint64_t, cudaStream_t st)
+{
+    if (n == 0) return cudaSuccess;
+    is_prime_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, out, n);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace gb
