@@ -124,8 +124,10 @@ __device__ void sieve_window(uint32_t *win, int64_t g0, uint32_t nw, const Sieve
         const uint32_t p = __ldg(sp.primes + pi);
         const uint64_t off = first_hit(p, __ldg(sp.magic + pi), o_lo, o_hi);
         if (off == UINT64_MAX) break;
-        for (uint64_t b = off + (uint64_t)lane * p; b < nbits; b += 32ull * p)
-            atomicAnd(win + (b >> 5), ~(1u << (b & 31)));
+        if (off >= nbits) continue;
+        const uint32_t stride = 32 * p;
+        for (uint32_t b = (uint32_t)off + lane * p; b < nbits; b += stride)
+            atomicAnd(win + (b >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b));   // ~(1 << b%32)
     }
     // Phase B: large primes, one thread per prime.
     const uint32_t b_begin = sp.i_big > sp.i_med ? sp.i_big : sp.i_med;
@@ -133,8 +135,8 @@ __device__ void sieve_window(uint32_t *win, int64_t g0, uint32_t nw, const Sieve
         const uint32_t p = __ldg(sp.primes + pi);
         const uint64_t off = first_hit(p, __ldg(sp.magic + pi), o_lo, o_hi);
         if (off == UINT64_MAX) break;
-        for (uint64_t b = off; b < nbits; b += p)
-            atomicAnd(win + (b >> 5), ~(1u << (b & 31)));
+        for (uint32_t b = (uint32_t)min(off, (uint64_t)nbits); b < nbits; b += p)
+            atomicAnd(win + (b >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b));
     }
 }
 
@@ -349,7 +351,103 @@ __device__ __forceinline__ void hist_add(uint32_t *sh_hist, int64_t *res, uint32
     else atomicAdd((unsigned long long *)(res + GB_R_HIST + bin), (unsigned long long)c);
 }
 
-template <bool DUMP>
+// ---- compile-time table of the first kUnroll odd primes (3, 5, 7, ..., 3673) ----
+// The fast path is fully unrolled over these, so every shift k = (p-1)/2, word
+// offset k/32 and bit offset k%32 is an immediate ("bitwise
+// AND/OR operations across aligned words").
+constexpr int kUnroll = 512;
+struct OddPrimeTable {
+    uint32_t p[kUnroll];
+};
+constexpr OddPrimeTable make_odd_primes()
+{
+    OddPrimeTable t{};
+    int c = 0;
+    for (uint32_t x = 3; c < kUnroll; x += 2) {
+        bool pr = true;
+        for (uint32_t d = 3; d * d <= x; d += 2)
+            if (x % d == 0) { pr = false; break; }
+        if (pr) t.p[c++] = x;
+    }
+    return t;
+}
+constexpr OddPrimeTable kOddPrimes = make_odd_primes();
+static_assert(kUnroll + 2 <= kHistSmem, "unrolled bins must live in the shared histogram");
+static_assert(kOddPrimes.p[0] == 3 && kOddPrimes.p[kUnroll - 1] == 3673, "odd prime table");
+
+struct Lane {
+    const uint32_t *w;   // &win[halo + local word]: O word of this lane's U word
+    uint32_t U;          // unresolved evens of the word
+    uint32_t word_sum;   // sum of p_min of bits resolved in the unrolled range
+    uint32_t lb;         // 1 + index of the last 8-prime block with a hit (0 = none)
+    uint32_t lu;         // U at the start of that block
+    uint32_t *dump_w;    // dump entry of bit 0 of the word (DUMP only)
+};
+
+// one candidate prime P = kOddPrimes.p[J] against one U word: S = O << K (K = (P-1)/2)
+template <int J, bool DUMP>
+__device__ __forceinline__ uint32_t mark_step(Lane &m)
+{
+    constexpr uint32_t P = kOddPrimes.p[J];
+    constexpr uint32_t K = P >> 1;
+    constexpr int A = (int)(K >> 5);
+    constexpr uint32_t B = K & 31;
+    const uint32_t S = __funnelshift_l(m.w[-(A + 1)], m.w[-A], B);
+    const uint32_t nw = m.U & S;          // n resolved now: n - P prime, no smaller p worked
+    m.U ^= nw;
+    const uint32_t c = __popc(nw);
+    m.word_sum += c * P;
+    if constexpr (DUMP) {
+        uint32_t x = nw;
+        while (x) {
+            const int b = __ffs(x) - 1;
+            x &= x - 1;
+            m.dump_w[b] = P;
+        }
+    }
+    return c;
+}
+
+// 8 primes, then the warp's per-prime counts go to the CTA histogram: two counts
+// per 32-bit register (16-bit fields: per word <= 32, per warp <= 1024), one
+// REDUX per pair, then lanes 0..7 add one bin each (bin of odd prime J = J + 2).
+template <int J, bool DUMP>
+__device__ __forceinline__ void mark_block8(Lane &m, uint32_t *hist, int lane)
+{
+    const uint32_t Ub = m.U;
+    const uint32_t c0 = mark_step<J + 0, DUMP>(m);
+    const uint32_t c1 = mark_step<J + 1, DUMP>(m);
+    const uint32_t c2 = mark_step<J + 2, DUMP>(m);
+    const uint32_t c3 = mark_step<J + 3, DUMP>(m);
+    const uint32_t c4 = mark_step<J + 4, DUMP>(m);
+    const uint32_t c5 = mark_step<J + 5, DUMP>(m);
+    const uint32_t c6 = mark_step<J + 6, DUMP>(m);
+    const uint32_t c7 = mark_step<J + 7, DUMP>(m);
+    if (m.U != Ub) {
+        m.lb = J / 8 + 1;
+        m.lu = Ub;
+    }
+    const uint32_t t0 = __reduce_add_sync(FULL, c0 | (c1 << 16));
+    const uint32_t t1 = __reduce_add_sync(FULL, c2 | (c3 << 16));
+    const uint32_t t2 = __reduce_add_sync(FULL, c4 | (c5 << 16));
+    const uint32_t t3 = __reduce_add_sync(FULL, c6 | (c7 << 16));
+    const uint32_t ts = (lane & 4) ? ((lane & 2) ? t3 : t2) : ((lane & 2) ? t1 : t0);
+    const uint32_t v = (lane & 1) ? (ts >> 16) : (ts & 0xffffu);
+    if (lane < 8 && v) atomicAdd(hist + J + 2 + lane, v);
+}
+
+template <int J, bool DUMP>
+__device__ __forceinline__ void mark_unrolled(Lane &m, uint32_t *hist, int lane)
+{
+    if constexpr (J + 8 <= kUnroll) {
+        if (!__any_sync(FULL, m.U != 0)) return;   // warp-level early exit, every 8 primes
+        mark_block8<J, DUMP>(m, hist, lane);
+        mark_unrolled<J + 8, DUMP>(m, hist, lane);
+    }
+}
+
+// UNROLL: n_cand >= kUnroll, so the whole unrolled table is inside the fast path.
+template <bool DUMP, bool UNROLL>
 __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
 {
     extern __shared__ uint32_t win[];          // halo + kTileWords words
@@ -357,6 +455,7 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     for (int i = tid; i < kHistSmem; i += blockDim.x) sh_hist[i] = 0;
     Acc acc;
+    uint32_t best_block = 0;                   // per warp: replay only rounds that can raise the max
     const uint64_t e_dump0 = a.e_lo;
 
     for (uint64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
@@ -380,18 +479,54 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
             }
             acc.evens += __popc(U);
             uint64_t word_sum = 0;
-            uint32_t lastp = 0, lastb = 0;
             if (U & 1u && u == 0) {           // n = 4: p_min = 2, the only even p (R2)
                 U &= ~1u;
                 word_sum += 2;
-                acc.verified += 1;
-                lastp = 2; lastb = 1;
                 atomicAdd(sh_hist + 1, 1u);
+                const uint64_t key = make_key(2, 4, a.origin);
+                if (key > acc.key) acc.key = key;
                 if (DUMP) a.dump[0 - e_dump0] = 2;
             }
             const uint32_t base = a.halo + (li < tw ? li : tw - 1);
-            // inverted loop: odd primes ascending; S = O shifted up by k = (p-1)/2
-            for (uint32_t j = 0; j < a.n_cand; ++j) {
+            uint32_t j0 = 0;
+            if constexpr (UNROLL) {
+                Lane m;
+                m.w = win + base;
+                m.U = U;
+                m.word_sum = 0;
+                m.lb = 0;
+                m.lu = 0;
+                m.dump_w = DUMP ? a.dump + ((int64_t)(u * 32) - (int64_t)e_dump0) : nullptr;
+                mark_unrolled<0, DUMP>(m, sh_hist, lane);
+                U = m.U;
+                word_sum += m.word_sum;
+                j0 = kUnroll;
+                // max p_min of the round: replay the last block with a hit, from the
+                // U saved at its start, only when the round can raise this warp's max
+                const uint32_t bstar = __reduce_max_sync(FULL, m.lb);
+                if (bstar && bstar >= best_block) {
+                    best_block = bstar;
+                    if (m.lb == bstar) {
+                        const uint32_t jr = (bstar - 1) * 8;
+                        uint32_t x = m.lu, lp = 0, lbits = 0;
+                        for (int i = 0; i < 8; ++i) {
+                            const uint32_t p = __ldg(a.sp.primes + jr + i);
+                            const int k = (int)(p >> 1);
+                            const uint32_t S = __funnelshift_l(m.w[-(k >> 5) - 1], m.w[-(k >> 5)], k);
+                            const uint32_t nw = x & S;
+                            x ^= nw;
+                            if (nw) { lp = p; lbits = nw; }
+                        }
+                        const uint64_t n = 4 + 2 * (u * 32 + (uint64_t)(__ffs(lbits) - 1));
+                        const uint64_t key = make_key(lp, n, a.origin);
+                        if (key > acc.key) acc.key = key;
+                    }
+                }
+            }
+            // generic runtime loop: the primes past the unrolled table (or all of
+            // them when p_max is below it)
+            uint32_t lastp = 0, lastb = 0;
+            for (uint32_t j = j0; j < a.n_cand; ++j) {
                 if (!__any_sync(FULL, U != 0)) break;
                 const uint32_t p = __ldg(a.sp.primes + j);
                 const uint32_t k = p >> 1;
@@ -402,7 +537,6 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
                 if (nw) {
                     U ^= nw;
                     word_sum += (uint64_t)c * p;
-                    acc.verified += c;
                     lastp = p; lastb = nw;
                     if (DUMP) {
                         uint32_t x = nw;
@@ -436,7 +570,6 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
                     U &= ~(1u << bit);
                     if (p) {
                         word_sum += p;
-                        acc.verified += 1;
                         hist_add(sh_hist, a.result, bin_of_prime(p, a.sp.primes, a.n_base), 1);
                         const uint64_t key = make_key(p, n, a.origin);
                         if (key > acc.key) acc.key = key;
@@ -451,7 +584,20 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
             acc.sum += word_sum;
             acc.chk += word_sum * u;          // sum p_min * floor((n-4)/64): u = e >> 5
         }
+        // per-tile flush of the shared histogram keeps its 32-bit bins exact
+        __syncthreads();
+        {
+            unsigned long long *R = (unsigned long long *)a.result;
+            for (int i = tid; i < kHistSmem; i += blockDim.x) {
+                const uint32_t v = sh_hist[i];
+                if (v) {
+                    atomicAdd(R + GB_R_HIST + i, (unsigned long long)v);
+                    sh_hist[i] = 0;
+                }
+            }
+        }
     }
+    acc.verified = acc.evens - acc.unres;
 
     // flush: warp-reduce then one atomic per warp per field
     __syncthreads();
@@ -481,9 +627,6 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
         if (ky) atomicMax(R + GB_R_MAX_KEY, ky);
         if (fr != UINT64_MAX) atomicMin(R + GB_R_FIRST_UNRESOLVED_N, fr);
     }
-    (void)warp;
-    for (int i = tid; i < kHistSmem; i += blockDim.x)
-        if (sh_hist[i]) atomicAdd(R + GB_R_HIST + i, (unsigned long long)sh_hist[i]);
 }
 
 __global__ void is_prime_kernel(const uint64_t *x, uint8_t *out, uint64_t n)
@@ -558,17 +701,22 @@ cudaError_t launch_result_finalize(int64_t *res, cudaStream_t st)
 
 cudaError_t configure_verify(size_t smem_max)
 {
-    cudaError_t e = cudaFuncSetAttribute(verify_kernel<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(verify_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem_max);
+    const int sm = (int)smem_max;
+    cudaError_t e = cudaFuncSetAttribute(verify_kernel<false, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(verify_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(verify_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(verify_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    return e;
 }
 
 int verify_blocks_per_sm(size_t smem)
 {
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, verify_kernel<false>, kThreads, smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, verify_kernel<false, true>, kThreads, smem) !=
         cudaSuccess)
         return 1;
     return nb < 1 ? 1 : nb;
@@ -576,10 +724,14 @@ int verify_blocks_per_sm(size_t smem)
 
 cudaError_t launch_verify(const VerifyArgs &a, int grid, size_t smem, cudaStream_t st)
 {
-    if (a.dump)
-        verify_kernel<true><<<grid, kThreads, smem, st>>>(a);
-    else
-        verify_kernel<false><<<grid, kThreads, smem, st>>>(a);
+    const bool unroll = a.n_cand >= (uint32_t)kUnroll;
+    if (a.dump) {
+        if (unroll) verify_kernel<true, true><<<grid, kThreads, smem, st>>>(a);
+        else verify_kernel<true, false><<<grid, kThreads, smem, st>>>(a);
+    } else {
+        if (unroll) verify_kernel<false, true><<<grid, kThreads, smem, st>>>(a);
+        else verify_kernel<false, false><<<grid, kThreads, smem, st>>>(a);
+    }
     count_launch();
     return cudaGetLastError();
 }

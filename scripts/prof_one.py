@@ -1,0 +1,31 @@
+#!/usr/bin/env python3
+"""One short launch of each libgb kernel for ncu (keeps replays cheap):
+gb_verify_range over the top 2^span integers of [4, N] and gb_sieve_segment over
+a window of the same size.  usage: python scripts/prof_one.py [--N 1e12] [--span 32]"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2603_02621_b200.verifier import Verifier  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--N", type=float, default=1e12)
+ap.add_argument("--span", type=int, default=32)
+ap.add_argument("--p-max", type=int, default=65521)
+ap.add_argument("--reps", type=int, default=1)
+a = ap.parse_args()
+N = int(a.N)
+v = Verifier(hi_max=N + 1, p_max=a.p_max)
+lo = N + 1 - (1 << a.span)
+r = v.new_result()
+for _ in range(a.reps):
+    v.verify(lo, N + 1, r)
+v.finalize(r)
+w = v.sieve_segment((lo - 3) // 128, (1 << a.span) // 128)
+torch.cuda.synchronize()
+d = v.decode(r)
+print({k: d[k] for k in ("evens", "verified", "fastpath_unresolved", "max_pmin", "max_pmin_n")})
