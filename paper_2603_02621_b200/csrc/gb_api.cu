@@ -27,10 +27,20 @@ uint64_t isqrt_u64(uint64_t x)
 
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
+constexpr uint64_t kMaxSms = 160;   // workspace sizing bound (B200: 148)
+
 struct Layout {
-    uint64_t R, bits_words, list_cap, n_blk;
-    uint64_t off_bits, off_primes, off_magic, off_blk, off_counter, off_res, off_dump, total;
+    uint64_t R, bits_words, list_cap, n_blk, carry_stride, carry_ctas;
+    uint64_t off_bits, off_primes, off_magic, off_tmod, off_carry, off_blk, off_counter, off_res,
+        off_dump, total;
 };
+
+// pi(x) upper bound (Rosser-Schoenfeld: pi(x) < 1.25506 x / ln x for x > 1) + slack
+uint64_t pi_upper(uint64_t x)
+{
+    if (x < 17) return 8;
+    return (uint64_t)(1.25506 * (double)x / __builtin_log((double)x)) + 64;
+}
 
 bool plan(uint64_t hi_max, uint32_t p_max, Layout &L)
 {
@@ -41,14 +51,19 @@ bool plan(uint64_t hi_max, uint32_t p_max, Layout &L)
     if (R > 0xFFFFFFFFull - 64) return false;   // primes are u32
     L.R = R;
     L.bits_words = ((R - 3) / 2) / 64 + 1;
-    // pi(x) < 1.25506 x / ln x (Rosser-Schoenfeld, x > 1)
-    double bound = 1.25506 * (double)R / __builtin_log((double)R);
-    L.list_cap = (uint64_t)bound + 64;
+    L.list_cap = pi_upper(R);
+    // carried offsets: one row per possible resident verify CTA, one u32 per sieving
+    // prime p <= min(isqrt(hi_max - 1), kCarryPrimeMax)
+    const uint64_t sq = isqrt_u64(hi_max - 1);
+    L.carry_stride = align_up(pi_upper(std::min<uint64_t>(sq, kCarryPrimeMax)), 64);
+    L.carry_ctas = 0;   // filled by the caller with the device's SM count
     L.n_blk = (L.bits_words + kScanBlockWords - 1) / kScanBlockWords;
     uint64_t o = 0;
     L.off_bits = o;    o = align_up(o + 8 * L.bits_words, 256);
     L.off_primes = o;  o = align_up(o + 4 * L.list_cap, 256);
     L.off_magic = o;   o = align_up(o + 8 * L.list_cap, 256);
+    L.off_tmod = o;    o = align_up(o + 8 * L.list_cap, 256);
+    L.off_carry = o;   o = align_up(o + 4 * L.carry_stride * (uint64_t)kMaxBlocksPerSm * kMaxSms, 256);
     L.off_blk = o;     o = align_up(o + 8 * (L.n_blk + 1), 256);
     L.off_counter = o; o = align_up(o + 256, 256);
     L.off_res = o;     o = align_up(o + 8 * (uint64_t)GB_RESULT_WORDS, 256);
@@ -71,6 +86,7 @@ SievePrimes sieve_primes(const gb_ctx *c, uint64_t sqrt_bound)
     SievePrimes sp;
     sp.primes = c->primes;
     sp.magic = c->magic;
+    sp.ptm = c->ptm;
     sp.i_med = count_le(c->h_primes, 31);
     sp.i_big = count_le(c->h_primes, kWarpPrimeMax);
     sp.n_use = count_le(c->h_primes, sqrt_bound);
@@ -137,6 +153,9 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
     c->bits_words = L.bits_words;
     c->primes = (uint32_t *)(ws + L.off_primes);
     c->magic = (uint64_t *)(ws + L.off_magic);
+    c->ptm = (uint2 *)(ws + L.off_tmod);
+    c->carry = (uint32_t *)(ws + L.off_carry);
+    c->carry_stride = L.carry_stride;
     c->blk = (uint64_t *)(ws + L.off_blk);
     c->counter = (uint32_t *)(ws + L.off_counter);
     c->res_scratch = (int64_t *)(ws + L.off_res);
@@ -145,10 +164,12 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
         delete c;
         return GB_ECUDA;
     }
+    if ((uint64_t)c->num_sms > kMaxSms) { delete c; return GB_EINTERNAL; }
+    c->carry_ctas = (uint32_t)(kMaxBlocksPerSm * c->num_sms);
     cudaStream_t st = S(stream);
     // K-BASE stage 1: seed primes <= isqrt(R) (with per-prime magic)
     const uint64_t s = isqrt_u64(L.R);
-    if (launch_seed(s, c->primes, c->magic, c->counter, st) != cudaSuccess) { delete c; return GB_ECUDA; }
+    if (launch_seed(s, c->primes, c->magic, c->ptm, c->counter, st) != cudaSuccess) { delete c; return GB_ECUDA; }
     uint32_t n_seed = 0;
     if (cudaMemcpyAsync(&n_seed, c->counter, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess) {
@@ -171,7 +192,7 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
     // K-BASE stage 3: compaction into the ascending list (+ magic)
     if (launch_count_bits(c->bits, L.bits_words, c->blk, st) != cudaSuccess ||
         launch_scan(c->blk, L.n_blk, st) != cudaSuccess ||
-        launch_scatter(c->bits, L.bits_words, c->blk, c->primes, c->magic, st) != cudaSuccess) {
+        launch_scatter(c->bits, L.bits_words, c->blk, c->primes, c->magic, c->ptm, st) != cudaSuccess) {
         delete c;
         return GB_ECUDA;
     }
@@ -285,7 +306,11 @@ gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_m
     const size_t smem = 4ull * (a.halo + kTileWords);
     const int per_sm = verify_blocks_per_sm(smem);
     const uint64_t max_grid = (uint64_t)per_sm * ctx->num_sms;
-    const int grid = (int)std::min<uint64_t>(a.n_tiles, max_grid);
+    const int grid = (int)std::min<uint64_t>(std::min<uint64_t>(a.n_tiles, max_grid), ctx->carry_ctas);
+    a.carry = ctx->carry;
+    a.carry_stride = ctx->carry_stride;
+    a.n_carry = std::min<uint32_t>(a.sp.n_use, count_le(ctx->h_primes, kCarryPrimeMax));
+    a.n_carry = (uint32_t)std::min<uint64_t>(a.n_carry, ctx->carry_stride);
     return launch_verify(a, grid, smem, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
 }
 

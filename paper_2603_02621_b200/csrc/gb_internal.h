@@ -19,11 +19,14 @@ constexpr uint32_t kWarpPrimeMax = 8192;   // primes <= this: one warp per prime
 constexpr int kTinyPrimes = 10;            // 3..31 sieved by word patterns
 constexpr uint64_t kDumpScratch = 1ull << 24;  // u32 entries of host-API dump scratch
 constexpr int kScanBlockWords = 2048;      // u64 words per K-BASE compaction block
+constexpr uint32_t kCarryPrimeMax = 1u << 21;  // verify CTAs carry sieve offsets of primes below
+constexpr int kMaxBlocksPerSm = 4;         // sizing bound for per-CTA carry storage
 
 // Arguments of the window sieve (K-SIEVE) shared by every caller.
 struct SievePrimes {
     const uint32_t *primes;   // odd primes ascending (3, 5, 7, ...)
     const uint64_t *magic;    // floor((2^64-1)/p) per prime
+    const uint2 *ptm;         // (p, (32*kTileWords) mod p) per prime
     uint32_t i_med;           // first index with p > 31 (word patterns below)
     uint32_t i_big;           // first index with p > kWarpPrimeMax
     uint32_t n_use;           // primes usable (p^2 beyond the window are skipped)
@@ -53,17 +56,20 @@ struct VerifyArgs {
     uint32_t n_base;          // odd primes in the resident list
     int64_t *result;
     uint32_t *dump;           // nullable
+    uint32_t *carry;          // per-CTA carried sieve offsets (nullable)
+    uint64_t carry_stride;    // u32 entries per CTA
+    uint32_t n_carry;         // primes [0, n_carry) carried
 };
 
 // Launchers (gb_kernels.cu).  Each returns the cudaGetLastError() of its launch.
-cudaError_t launch_seed(uint64_t s, uint32_t *primes, uint64_t *magic, uint32_t *d_count,
-                        cudaStream_t st);
+cudaError_t launch_seed(uint64_t s, uint32_t *primes, uint64_t *magic, uint2 *ptm,
+                        uint32_t *d_count, cudaStream_t st);
 cudaError_t launch_segment(const SegmentArgs &a, cudaStream_t st);
 cudaError_t launch_count_bits(const uint64_t *bits, uint64_t n_words, uint64_t *blk,
                               cudaStream_t st);
 cudaError_t launch_scan(uint64_t *blk, uint64_t n_blk, cudaStream_t st);
 cudaError_t launch_scatter(const uint64_t *bits, uint64_t n_words, const uint64_t *blk,
-                           uint32_t *primes, uint64_t *magic, cudaStream_t st);
+                           uint32_t *primes, uint64_t *magic, uint2 *ptm, cudaStream_t st);
 cudaError_t launch_result_init(int64_t *res, cudaStream_t st);
 cudaError_t launch_result_finalize(int64_t *res, cudaStream_t st);
 cudaError_t launch_verify(const VerifyArgs &a, int grid, size_t smem, cudaStream_t st);
@@ -87,6 +93,10 @@ struct gb_ctx {
     uint64_t bits_words;
     uint32_t *primes;      // odd primes <= R
     uint64_t *magic;
+    uint2 *ptm;            // (p, (32*kTileWords) mod p)
+    uint32_t *carry;       // verify-kernel carried offsets: carry_ctas x carry_stride
+    uint64_t carry_stride;
+    uint32_t carry_ctas;
     uint64_t *blk;         // K-BASE scratch
     uint32_t *counter;     // K-BASE scratch
     int64_t *res_scratch;  // host API result

@@ -61,6 +61,23 @@ __host__ __device__ constexpr uint32_t tiny_pattern(int P, int i = 0)
 {
     return i >= 32 ? 0u : ((1u << i) | tiny_pattern(P, i + P));
 }
+// Carried sieve state of one persistent CTA: off[i] = first hit of prime i in the
+// NEXT window, relative to its start (valid for primes active in this window).
+constexpr uint32_t kTileBits = 32u * kTileWords;
+struct Carry {
+    uint32_t *off;
+    uint32_t n_carry;
+    bool have_prev;
+};
+
+// first hit >= kTileBits of the progression off, off + p, ... minus kTileBits
+__device__ __forceinline__ uint32_t next_tile_off(uint32_t off, uint32_t p, uint32_t tm)
+{
+    if (off >= kTileBits) return off - kTileBits;
+    uint32_t om = off < p ? off : off % p;       // off >= p only when p^2 fell in this window
+    return om >= tm ? om - tm : om + p - tm;
+}
+
 template <int P>
 struct Tiny {
     static constexpr uint32_t value = tiny_pattern(P);
@@ -72,7 +89,8 @@ struct Tiny {
 // every q whose square root is covered by sp (callers guarantee it).
 // Ends WITHOUT a barrier; callers __syncthreads() before reading `win`.
 // ---------------------------------------------------------------------------
-__device__ void sieve_window(uint32_t *win, int64_t g0, uint32_t nw, const SievePrimes &sp)
+__device__ void sieve_window(uint32_t *win, int64_t g0, uint32_t nw, const SievePrimes &sp,
+                             const Carry *cy = nullptr)
 {
     const int tid = threadIdx.x, nt = blockDim.x;
     // Phase T: primes 3..31 by shifted word patterns.  For word g the first
@@ -118,25 +136,85 @@ __device__ void sieve_window(uint32_t *win, int64_t g0, uint32_t nw, const Sieve
     const int64_t o_hi = (g0 + (int64_t)nw) * 32;
     const uint32_t nbits = nw * 32;
     const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
-    // Phase M: medium primes (31 < p <= kWarpPrimeMax), one warp per prime.
-    const uint32_t m_end = sp.i_big < sp.n_use ? sp.i_big : sp.n_use;
-    for (uint32_t pi = sp.i_med + warp; pi < m_end; pi += nwarps) {
-        const uint32_t p = __ldg(sp.primes + pi);
-        const uint64_t off = first_hit(p, __ldg(sp.magic + pi), o_lo, o_hi);
-        if (off == UINT64_MAX) break;
-        if (off >= nbits) continue;
-        const uint32_t stride = 32 * p;
-        for (uint32_t b = (uint32_t)off + lane * p; b < nbits; b += stride)
-            atomicAnd(win + (b >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b));   // ~(1 << b%32)
+    // With a carry context (persistent verify CTAs walking consecutive tiles) the
+    // first hit of every active prime comes from the previous tile instead of a
+    // 64-bit modulo: the window of tile t+1 starts kTileBits above that of tile t.
+    // `steady`: every sieving prime was active in the previous window too, so every
+    // carried offset is valid and < p (no p^2 checks, no modulo at all).
+    bool steady = false;
+    if (cy && cy->have_prev && sp.n_use > 0 && sp.n_use <= cy->n_carry) {
+        const uint32_t pl = __ldg(sp.primes + sp.n_use - 1);
+        steady = (int64_t)(((uint64_t)pl * pl - 3) >> 1) < o_lo - (int64_t)kTileBits;
     }
-    // Phase B: large primes, one thread per prime.
+    // Phase M: medium primes (31 < p <= kWarpPrimeMax), one warp per prime.  Warp w
+    // takes primes i_med + w + nwarps*(32k + l); lane l computes the start offset of
+    // the k-th batch's l-th prime, then the warp marks the 32 primes one by one.
+    const uint32_t m_end = sp.i_big < sp.n_use ? sp.i_big : sp.n_use;
+    for (uint32_t bi = sp.i_med + warp; bi < m_end; bi += 32u * nwarps) {
+        const uint32_t pi = bi + (uint32_t)lane * nwarps;
+        uint32_t p = 0, off = 0xFFFFFFFFu;
+        if (pi < m_end) {
+            const uint2 pt = __ldg(sp.ptm + pi);
+            p = pt.x;
+            if (steady) {
+                off = cy->off[pi];
+                cy->off[pi] = off >= pt.y ? off - pt.y : off + p - pt.y;
+            } else {
+                const int64_t opp = (int64_t)(((uint64_t)p * p - 3) >> 1);
+                if (opp < o_hi) {
+                    const bool carried = cy && pi < cy->n_carry;
+                    uint64_t o64;
+                    if (carried && cy->have_prev && opp < o_hi - (int64_t)kTileBits) o64 = cy->off[pi];
+                    else o64 = first_hit(p, __ldg(sp.magic + pi), o_lo, o_hi);
+                    off = (uint32_t)o64;
+                    if (carried) cy->off[pi] = next_tile_off(off, p, pt.y);
+                }
+            }
+        }
+        const uint32_t n_here = min(32u, (m_end - bi + nwarps - 1) / nwarps);
+        for (uint32_t i = 0; i < n_here; ++i) {
+            const uint32_t pp = __shfl_sync(FULL, p, i);
+            const uint32_t oo = __shfl_sync(FULL, off, i);
+            if (oo >= nbits) continue;
+            const uint32_t stride = 32 * pp;
+            for (uint32_t b = oo + lane * pp; b < nbits; b += stride)
+                atomicAnd(win + (b >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b));   // ~(1 << b%32)
+        }
+    }
+    // Phase B: large primes, one thread per prime (next prime's loads issued early).
     const uint32_t b_begin = sp.i_big > sp.i_med ? sp.i_big : sp.i_med;
-    for (uint32_t pi = b_begin + tid; pi < sp.n_use; pi += nt) {
-        const uint32_t p = __ldg(sp.primes + pi);
-        const uint64_t off = first_hit(p, __ldg(sp.magic + pi), o_lo, o_hi);
-        if (off == UINT64_MAX) break;
-        for (uint32_t b = (uint32_t)min(off, (uint64_t)nbits); b < nbits; b += p)
-            atomicAnd(win + (b >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b));
+    if (steady) {
+        uint32_t pi = b_begin + tid;
+        uint2 pt = make_uint2(0, 0);
+        uint32_t off = 0;
+        if (pi < sp.n_use) { pt = __ldg(sp.ptm + pi); off = cy->off[pi]; }
+        for (; pi < sp.n_use; pi += nt) {
+            const uint32_t pn = pi + nt;
+            uint2 ptn = make_uint2(0, 0);
+            uint32_t offn = 0;
+            if (pn < sp.n_use) { ptn = __ldg(sp.ptm + pn); offn = cy->off[pn]; }
+            const uint32_t p = pt.x;
+            for (uint32_t b = off; b < nbits; b += p)
+                atomicAnd(win + (b >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b));
+            cy->off[pi] = off >= pt.y ? off - pt.y : off + p - pt.y;
+            pt = ptn;
+            off = offn;
+        }
+    } else {
+        for (uint32_t pi = b_begin + tid; pi < sp.n_use; pi += nt) {
+            const uint2 pt = __ldg(sp.ptm + pi);
+            const uint32_t p = pt.x;
+            const int64_t opp = (int64_t)(((uint64_t)p * p - 3) >> 1);
+            if (opp >= o_hi) break;
+            const bool carried = cy && pi < cy->n_carry;
+            uint64_t off;
+            if (carried && cy->have_prev && opp < o_hi - (int64_t)kTileBits) off = cy->off[pi];
+            else off = first_hit(p, __ldg(sp.magic + pi), o_lo, o_hi);
+            uint32_t b = (uint32_t)min(off, (uint64_t)nbits);
+            for (; b < nbits; b += p)
+                atomicAnd(win + (b >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b));
+            if (carried) cy->off[pi] = next_tile_off((uint32_t)off, p, pt.y);
+        }
     }
 }
 
@@ -165,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) segment_kernel(SegmentArgs a)
 // K-BASE stage 1: primes <= s (s <= 65535) in one CTA, byte sieve in smem.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) seed_kernel(uint32_t s, uint32_t *primes, uint64_t *magic,
-                                                    uint32_t *d_count)
+                                                    uint2 *ptm, uint32_t *d_count)
 {
     extern __shared__ uint8_t flag[];
     for (uint32_t i = threadIdx.x; i <= s; i += blockDim.x) flag[i] = (i >= 2);
@@ -185,7 +263,10 @@ __global__ void __launch_bounds__(1024) seed_kernel(uint32_t s, uint32_t *primes
         *d_count = c;
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) magic[i] = ~0ull / primes[i];
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+        magic[i] = ~0ull / primes[i];
+        ptm[i] = make_uint2(primes[i], kTileBits % primes[i]);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -231,7 +312,7 @@ __global__ void __launch_bounds__(1024) scan_kernel(uint64_t *blk, uint64_t n)
 
 __global__ void __launch_bounds__(256) scatter_kernel(const uint64_t *bits, uint64_t n_words,
                                                       const uint64_t *blk, uint32_t *primes,
-                                                      uint64_t *magic)
+                                                      uint64_t *magic, uint2 *ptm)
 {
     // each thread owns kScanBlockWords/256 = 8 consecutive words of this block
     constexpr int per = kScanBlockWords / 256;
@@ -260,6 +341,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint64_t *bits, uint
             const uint64_t q = 3 + 2 * (64 * w + (uint64_t)b);
             primes[idx] = (uint32_t)q;
             magic[idx] = ~0ull / q;
+            ptm[idx] = make_uint2((uint32_t)q, (uint32_t)(kTileBits % q));
             ++idx;
         }
     }
@@ -446,143 +528,273 @@ __device__ __forceinline__ void mark_unrolled(Lane &m, uint32_t *hist, int lane)
     }
 }
 
+// Phase 1 of the mark: the first kPhase1 primes for two words per lane (every word
+// needs them: the max p_min index of a 32-even word is rarely below 40), no exit
+// checks; the per-prime counts of both words share one REDUX.
+constexpr int kPhase1 = 64;
+constexpr int kQueue = 128;                  // per-warp survivor queue (entries)
+
+template <int J, bool DUMP>
+__device__ __forceinline__ void p1_block8(Lane &m0, Lane &m1, uint32_t *hist, int lane)
+{
+    const uint32_t U0 = m0.U, U1 = m1.U;
+    uint32_t c[8];
+    c[0] = mark_step<J + 0, DUMP>(m0); c[0] += mark_step<J + 0, DUMP>(m1);
+    c[1] = mark_step<J + 1, DUMP>(m0); c[1] += mark_step<J + 1, DUMP>(m1);
+    c[2] = mark_step<J + 2, DUMP>(m0); c[2] += mark_step<J + 2, DUMP>(m1);
+    c[3] = mark_step<J + 3, DUMP>(m0); c[3] += mark_step<J + 3, DUMP>(m1);
+    c[4] = mark_step<J + 4, DUMP>(m0); c[4] += mark_step<J + 4, DUMP>(m1);
+    c[5] = mark_step<J + 5, DUMP>(m0); c[5] += mark_step<J + 5, DUMP>(m1);
+    c[6] = mark_step<J + 6, DUMP>(m0); c[6] += mark_step<J + 6, DUMP>(m1);
+    c[7] = mark_step<J + 7, DUMP>(m0); c[7] += mark_step<J + 7, DUMP>(m1);
+    if (m0.U != U0) { m0.lb = J / 8 + 1; m0.lu = U0; }
+    if (m1.U != U1) { m1.lb = J / 8 + 1; m1.lu = U1; }
+    // per warp and prime <= 2048 hits: 16-bit fields
+    const uint32_t t0 = __reduce_add_sync(FULL, c[0] + (c[1] << 16));
+    const uint32_t t1 = __reduce_add_sync(FULL, c[2] + (c[3] << 16));
+    const uint32_t t2 = __reduce_add_sync(FULL, c[4] + (c[5] << 16));
+    const uint32_t t3 = __reduce_add_sync(FULL, c[6] + (c[7] << 16));
+    const uint32_t ts = (lane & 4) ? ((lane & 2) ? t3 : t2) : ((lane & 2) ? t1 : t0);
+    const uint32_t v = (lane & 1) ? (ts >> 16) : (ts & 0xffffu);
+    if (lane < 8 && v) atomicAdd(hist + J + 2 + lane, v);
+}
+
+template <int J, bool DUMP>
+__device__ __forceinline__ void p1_blocks(Lane &m0, Lane &m1, uint32_t *hist, int lane)
+{
+    if constexpr (J < kPhase1) {
+        p1_block8<J, DUMP>(m0, m1, hist, lane);
+        p1_blocks<J + 8, DUMP>(m0, m1, hist, lane);
+    }
+}
+
+// max p_min among the hits recorded in m.lb/m.lu: replay that 8-prime block from
+// the U saved at its start (only lanes holding the warp's latest block, and only
+// when it can raise this warp's running maximum)
+__device__ __forceinline__ void replay_key(const Lane &m, uint64_t u, const VerifyArgs &a,
+                                           uint32_t &best_block, Acc &acc)
+{
+    const uint32_t bstar = __reduce_max_sync(FULL, m.lb);
+    if (bstar == 0 || bstar < best_block) return;
+    best_block = bstar;
+    if (m.lb != bstar) return;
+    const uint32_t jr = (bstar - 1) * 8;
+    uint32_t x = m.lu, lp = 0, lbits = 0;
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t p = __ldg(a.sp.primes + jr + i);
+        const int k = (int)(p >> 1);
+        const uint32_t S = __funnelshift_l(m.w[-(k >> 5) - 1], m.w[-(k >> 5)], k);
+        const uint32_t nw = x & S;
+        x ^= nw;
+        if (nw) { lp = p; lbits = nw; }
+    }
+    const uint64_t n = 4 + 2 * (u * 32 + (uint64_t)(__ffs(lbits) - 1));
+    const uint64_t key = make_key(lp, n, a.origin);
+    if (key > acc.key) acc.key = key;
+}
+
+// Primes past the unrolled range (runtime loop), then the exhaustive on-GPU
+// fallback for whatever the fast path left; folds the word into acc.
+template <bool DUMP>
+__device__ __forceinline__ void finish_word(uint32_t U, uint64_t word_sum, uint32_t j0, uint32_t base,
+                                            uint64_t u, const uint32_t *win, uint32_t *sh_hist,
+                                            const VerifyArgs &a, Acc &acc, int lane)
+{
+    const uint64_t e_dump0 = a.e_lo;
+    uint32_t lastp = 0, lastb = 0;
+    for (uint32_t j = j0; j < a.n_cand; ++j) {
+        if (!__any_sync(FULL, U != 0)) break;
+        const uint32_t p = __ldg(a.sp.primes + j);
+        const uint32_t k = p >> 1;
+        const uint32_t wa = k >> 5, bb = k & 31;
+        const uint32_t S = __funnelshift_l(win[base - wa - 1], win[base - wa], bb);
+        const uint32_t nw = U & S;
+        const uint32_t c = __popc(nw);
+        if (nw) {
+            U ^= nw;
+            word_sum += (uint64_t)c * p;
+            lastp = p; lastb = nw;
+            if (DUMP) {
+                uint32_t x = nw;
+                while (x) {
+                    const int b = __ffs(x) - 1;
+                    x &= x - 1;
+                    a.dump[u * 32 + b - e_dump0] = p;
+                }
+            }
+        }
+        const uint32_t tot = __reduce_add_sync(FULL, c);
+        if (lane == 0 && tot) hist_add(sh_hist, a.result, j + 2, tot);
+    }
+    if (lastp) {
+        const uint64_t n = 4 + 2 * (u * 32 + (uint64_t)(__ffs(lastb) - 1));
+        const uint64_t key = make_key(lastp, n, a.origin);
+        if (key > acc.key) acc.key = key;
+    }
+    acc.fast_unres += __popc(U);
+    while (true) {
+        const uint32_t m = __ballot_sync(FULL, U != 0);
+        if (!m) break;
+        const int L = __ffs(m) - 1;
+        const uint32_t lw = __shfl_sync(FULL, U, L);
+        const uint64_t uL = __shfl_sync(FULL, u, L);
+        const int bit = __ffs(lw) - 1;
+        const uint64_t n = 4 + 2 * (uL * 32 + (uint64_t)bit);
+        const uint64_t p = fallback_scan(n, a.p_fallback, a.cap, a.base_bits, a.R);
+        if (lane == L) {
+            U &= ~(1u << bit);
+            if (p) {
+                word_sum += p;
+                hist_add(sh_hist, a.result, bin_of_prime(p, a.sp.primes, a.n_base), 1);
+                const uint64_t key = make_key(p, n, a.origin);
+                if (key > acc.key) acc.key = key;
+            } else {
+                acc.unres += 1;
+                hist_add(sh_hist, a.result, 0, 1);
+                if (n < acc.first_unres) acc.first_unres = n;
+            }
+            if (DUMP) a.dump[uL * 32 + bit - e_dump0] = (uint32_t)p;
+        }
+    }
+    acc.sum += word_sum;
+    acc.chk += word_sum * u;                 // sum p_min * floor((n-4)/64): u = e >> 5
+}
+
+__device__ __forceinline__ uint32_t valid_mask(uint64_t u, const VerifyArgs &a)
+{
+    const uint64_t eb = u * 32;
+    uint32_t U = FULL;
+    if (eb < a.e_lo) U = (a.e_lo - eb >= 32) ? 0u : (U << (a.e_lo - eb));
+    if (eb + 32 > a.e_hi) U &= (a.e_hi <= eb) ? 0u : (FULL >> (eb + 32 - a.e_hi));
+    return U;
+}
+
+// n = 4 (bit 0 of word 0): p_min = 2, the only even p (reading R2)
+template <bool DUMP>
+__device__ __forceinline__ uint32_t take_n4(uint32_t U, uint64_t u, uint32_t *sh_hist,
+                                            const VerifyArgs &a, Acc &acc)
+{
+    if ((U & 1u) && u == 0) {
+        U &= ~1u;
+        acc.sum += 2;
+        atomicAdd(sh_hist + 1, 1u);
+        const uint64_t key = make_key(2, 4, a.origin);
+        if (key > acc.key) acc.key = key;
+        if (DUMP) a.dump[0 - a.e_lo] = 2;
+    }
+    return U;
+}
+
 // UNROLL: n_cand >= kUnroll, so the whole unrolled table is inside the fast path.
 template <bool DUMP, bool UNROLL>
 __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
 {
     extern __shared__ uint32_t win[];          // halo + kTileWords words
     __shared__ uint32_t sh_hist[kHistSmem];
+    __shared__ uint32_t q_li[kThreads / 32][kQueue];
+    __shared__ uint32_t q_U[kThreads / 32][kQueue];
+    __shared__ uint32_t sh_next;               // next phase-1 round of the tile
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     for (int i = tid; i < kHistSmem; i += blockDim.x) sh_hist[i] = 0;
     Acc acc;
     uint32_t best_block = 0;                   // per warp: replay only rounds that can raise the max
     const uint64_t e_dump0 = a.e_lo;
+    // contiguous run of tiles per CTA, so the sieve can carry its offsets
+    const uint64_t t_begin = (uint64_t)blockIdx.x * a.n_tiles / gridDim.x;
+    const uint64_t t_end = (uint64_t)(blockIdx.x + 1) * a.n_tiles / gridDim.x;
+    Carry cy;
+    cy.off = a.carry ? a.carry + (uint64_t)blockIdx.x * a.carry_stride : nullptr;
+    cy.n_carry = a.carry ? a.n_carry : 0;
+    cy.have_prev = false;
 
-    for (uint64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+    for (uint64_t tile = t_begin; tile < t_end; ++tile) {
         const uint64_t u0 = a.u_first + tile * kTileWords;
         const uint32_t tw = (uint32_t)min((uint64_t)kTileWords, a.u_end - u0);
         __syncthreads();                      // previous tile fully consumed
-        sieve_window(win, (int64_t)u0 - a.halo, a.halo + tw, a.sp);
+        if (tid == 0) sh_next = 0;
+        sieve_window(win, (int64_t)u0 - a.halo, a.halo + tw, a.sp, a.carry ? &cy : nullptr);
+        cy.have_prev = true;
         __syncthreads();
 
-        // rounds of 32 words, one word per lane, interleaved over warps
-        const uint32_t n_rounds = (tw + 31) >> 5;
-        for (uint32_t r = warp; r < n_rounds; r += nwarps) {
-            const uint32_t li = r * 32 + lane;
-            const uint64_t u = u0 + li;
-            uint32_t U = 0;
-            if (li < tw) {
-                const uint64_t eb = u * 32;
-                U = FULL;
-                if (eb < a.e_lo) U = (a.e_lo - eb >= 32) ? 0u : (U << (a.e_lo - eb));
-                if (eb + 32 > a.e_hi) U &= (a.e_hi <= eb) ? 0u : (FULL >> (eb + 32 - a.e_hi));
-            }
-            acc.evens += __popc(U);
-            uint64_t word_sum = 0;
-            if (U & 1u && u == 0) {           // n = 4: p_min = 2, the only even p (R2)
-                U &= ~1u;
-                word_sum += 2;
-                atomicAdd(sh_hist + 1, 1u);
-                const uint64_t key = make_key(2, 4, a.origin);
-                if (key > acc.key) acc.key = key;
-                if (DUMP) a.dump[0 - e_dump0] = 2;
-            }
-            const uint32_t base = a.halo + (li < tw ? li : tw - 1);
-            uint32_t j0 = 0;
-            if constexpr (UNROLL) {
+        if constexpr (UNROLL) {
+            // phase 1: rounds of 64 words (2 per lane) through the first kPhase1 primes,
+            // handed out dynamically; survivors queue per warp; batches of 32 go
+            // through phase 2 (the rest of the unrolled table with warp exits)
+            uint32_t qn = 0;
+            const uint32_t n_rounds = (tw + 63) >> 6;
+            auto phase2 = [&](uint32_t take) {
+                const uint32_t e = qn - take;
+                uint32_t li = 0, U = 0;
+                if ((uint32_t)lane < take) { li = q_li[warp][e + lane]; U = q_U[warp][e + lane]; }
+                __syncwarp();
+                qn = e;
+                const uint64_t u = u0 + li;
                 Lane m;
-                m.w = win + base;
+                m.w = win + a.halo + li;
                 m.U = U;
                 m.word_sum = 0;
-                m.lb = 0;
-                m.lu = 0;
+                m.lb = 0; m.lu = 0;
                 m.dump_w = DUMP ? a.dump + ((int64_t)(u * 32) - (int64_t)e_dump0) : nullptr;
-                mark_unrolled<0, DUMP>(m, sh_hist, lane);
-                U = m.U;
-                word_sum += m.word_sum;
-                j0 = kUnroll;
-                // max p_min of the round: replay the last block with a hit, from the
-                // U saved at its start, only when the round can raise this warp's max
-                const uint32_t bstar = __reduce_max_sync(FULL, m.lb);
-                if (bstar && bstar >= best_block) {
-                    best_block = bstar;
-                    if (m.lb == bstar) {
-                        const uint32_t jr = (bstar - 1) * 8;
-                        uint32_t x = m.lu, lp = 0, lbits = 0;
-                        for (int i = 0; i < 8; ++i) {
-                            const uint32_t p = __ldg(a.sp.primes + jr + i);
-                            const int k = (int)(p >> 1);
-                            const uint32_t S = __funnelshift_l(m.w[-(k >> 5) - 1], m.w[-(k >> 5)], k);
-                            const uint32_t nw = x & S;
-                            x ^= nw;
-                            if (nw) { lp = p; lbits = nw; }
-                        }
-                        const uint64_t n = 4 + 2 * (u * 32 + (uint64_t)(__ffs(lbits) - 1));
-                        const uint64_t key = make_key(lp, n, a.origin);
-                        if (key > acc.key) acc.key = key;
-                    }
-                }
-            }
-            // generic runtime loop: the primes past the unrolled table (or all of
-            // them when p_max is below it)
-            uint32_t lastp = 0, lastb = 0;
-            for (uint32_t j = j0; j < a.n_cand; ++j) {
-                if (!__any_sync(FULL, U != 0)) break;
-                const uint32_t p = __ldg(a.sp.primes + j);
-                const uint32_t k = p >> 1;
-                const uint32_t wa = k >> 5, bb = k & 31;
-                const uint32_t S = __funnelshift_l(win[base - wa - 1], win[base - wa], bb);
-                const uint32_t nw = U & S;
-                const uint32_t c = __popc(nw);
-                if (nw) {
-                    U ^= nw;
-                    word_sum += (uint64_t)c * p;
-                    lastp = p; lastb = nw;
-                    if (DUMP) {
-                        uint32_t x = nw;
-                        while (x) {
-                            const int b = __ffs(x) - 1;
-                            x &= x - 1;
-                            a.dump[u * 32 + b - e_dump0] = p;
-                        }
-                    }
-                }
-                const uint32_t tot = __reduce_add_sync(FULL, c);
-                if (lane == 0 && tot) hist_add(sh_hist, a.result, j + 2, tot);
-            }
-            if (lastp) {
-                const uint64_t n = 4 + 2 * (u * 32 + (uint64_t)(__ffs(lastb) - 1));
-                const uint64_t key = make_key(lastp, n, a.origin);
-                if (key > acc.key) acc.key = key;
-            }
-            // exhaustive fallback for whatever the fast path left (rare)
-            acc.fast_unres += __popc(U);
+                mark_unrolled<kPhase1, DUMP>(m, sh_hist, lane);
+                replay_key(m, u, a, best_block, acc);
+                finish_word<DUMP>(m.U, m.word_sum, kUnroll, a.halo + li, u, win, sh_hist, a, acc, lane);
+            };
             while (true) {
-                const uint32_t m = __ballot_sync(FULL, U != 0);
-                if (!m) break;
-                const int L = __ffs(m) - 1;
-                const uint32_t lw = __shfl_sync(FULL, U, L);
-                const uint64_t uL = __shfl_sync(FULL, u, L);
-                const int bit = __ffs(lw) - 1;
-                const uint64_t n = 4 + 2 * (uL * 32 + (uint64_t)bit);
-                const uint64_t p = fallback_scan(n, a.p_fallback, a.cap, a.base_bits, a.R);
-                if (lane == L) {
-                    U &= ~(1u << bit);
-                    if (p) {
-                        word_sum += p;
-                        hist_add(sh_hist, a.result, bin_of_prime(p, a.sp.primes, a.n_base), 1);
-                        const uint64_t key = make_key(p, n, a.origin);
-                        if (key > acc.key) acc.key = key;
-                    } else {
-                        acc.unres += 1;
-                        hist_add(sh_hist, a.result, 0, 1);
-                        if (n < acc.first_unres) acc.first_unres = n;
-                    }
-                    if (DUMP) a.dump[uL * 32 + bit - e_dump0] = (uint32_t)p;
+                uint32_t r = 0;
+                if (lane == 0) r = atomicAdd(&sh_next, 1u);
+                r = __shfl_sync(FULL, r, 0);
+                if (r >= n_rounds) break;
+                const uint32_t li0 = r * 64 + lane, li1 = li0 + 32;
+                const uint64_t ua = u0 + li0, ub = u0 + li1;
+                uint32_t Ua = li0 < tw ? valid_mask(ua, a) : 0u;
+                uint32_t Ub = li1 < tw ? valid_mask(ub, a) : 0u;
+                acc.evens += __popc(Ua) + __popc(Ub);
+                Ua = take_n4<DUMP>(Ua, ua, sh_hist, a, acc);
+                Lane m0, m1;
+                m0.w = win + a.halo + (li0 < tw ? li0 : tw - 1);
+                m1.w = win + a.halo + (li1 < tw ? li1 : tw - 1);
+                m0.U = Ua; m1.U = Ub;
+                m0.word_sum = m1.word_sum = 0;
+                m0.lb = m1.lb = 0; m0.lu = m1.lu = 0;
+                m0.dump_w = DUMP ? a.dump + ((int64_t)(ua * 32) - (int64_t)e_dump0) : nullptr;
+                m1.dump_w = DUMP ? a.dump + ((int64_t)(ub * 32) - (int64_t)e_dump0) : nullptr;
+                p1_blocks<0, DUMP>(m0, m1, sh_hist, lane);
+                acc.sum += (uint64_t)m0.word_sum + m1.word_sum;
+                acc.chk += (uint64_t)m0.word_sum * ua + (uint64_t)m1.word_sum * ub;
+                // max key of the phase-1 hits of this round (both words may hold it)
+                replay_key(m0, ua, a, best_block, acc);
+                replay_key(m1, ub, a, best_block, acc);
+                // enqueue survivors
+                uint32_t bal = __ballot_sync(FULL, m0.U != 0);
+                if (m0.U) {
+                    const uint32_t pos = qn + __popc(bal & ((1u << lane) - 1));
+                    q_li[warp][pos] = li0;
+                    q_U[warp][pos] = m0.U;
                 }
+                qn += __popc(bal);
+                bal = __ballot_sync(FULL, m1.U != 0);
+                if (m1.U) {
+                    const uint32_t pos = qn + __popc(bal & ((1u << lane) - 1));
+                    q_li[warp][pos] = li1;
+                    q_U[warp][pos] = m1.U;
+                }
+                qn += __popc(bal);
+                __syncwarp();
+                while (qn >= 32) phase2(32);
             }
-            acc.sum += word_sum;
-            acc.chk += word_sum * u;          // sum p_min * floor((n-4)/64): u = e >> 5
+            if (qn > 0) phase2(qn);
+        } else {
+            // p_max below the unrolled table: runtime loop for every word (tests)
+            const uint32_t n_rounds = (tw + 31) >> 5;
+            for (uint32_t r = warp; r < n_rounds; r += nwarps) {
+                const uint32_t li = r * 32 + lane;
+                const uint64_t u = u0 + li;
+                uint32_t U = li < tw ? valid_mask(u, a) : 0u;
+                acc.evens += __popc(U);
+                U = take_n4<DUMP>(U, u, sh_hist, a, acc);
+                finish_word<DUMP>(U, 0, 0, a.halo + (li < tw ? li : tw - 1), u, win, sh_hist, a, acc,
+                                  lane);
+            }
         }
         // per-tile flush of the shared histogram keeps its 32-bit bins exact
         __syncthreads();
@@ -600,7 +812,6 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
     acc.verified = acc.evens - acc.unres;
 
     // flush: warp-reduce then one atomic per warp per field
-    __syncthreads();
     auto wsum = [&](uint64_t v) {
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
         return v;
@@ -638,13 +849,13 @@ __global__ void is_prime_kernel(const uint64_t *x, uint8_t *out, uint64_t n)
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-cudaError_t launch_seed(uint64_t s, uint32_t *primes, uint64_t *magic, uint32_t *d_count,
-                        cudaStream_t st)
+cudaError_t launch_seed(uint64_t s, uint32_t *primes, uint64_t *magic, uint2 *ptm,
+                        uint32_t *d_count, cudaStream_t st)
 {
     static const cudaError_t attr = cudaFuncSetAttribute(
         seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 16);
     if (attr != cudaSuccess) return attr;
-    seed_kernel<<<1, 1024, (size_t)s + 1, st>>>((uint32_t)s, primes, magic, d_count);
+    seed_kernel<<<1, 1024, (size_t)s + 1, st>>>((uint32_t)s, primes, magic, ptm, d_count);
     count_launch();
     return cudaGetLastError();
 }
@@ -677,10 +888,10 @@ cudaError_t launch_scan(uint64_t *blk, uint64_t n_blk, cudaStream_t st)
 }
 
 cudaError_t launch_scatter(const uint64_t *bits, uint64_t n_words, const uint64_t *blk,
-                           uint32_t *primes, uint64_t *magic, cudaStream_t st)
+                           uint32_t *primes, uint64_t *magic, uint2 *ptm, cudaStream_t st)
 {
     const uint64_t nb = (n_words + kScanBlockWords - 1) / kScanBlockWords;
-    scatter_kernel<<<(unsigned)nb, 256, 0, st>>>(bits, n_words, blk, primes, magic);
+    scatter_kernel<<<(unsigned)nb, 256, 0, st>>>(bits, n_words, blk, primes, magic, ptm);
     count_launch();
     return cudaGetLastError();
 }
