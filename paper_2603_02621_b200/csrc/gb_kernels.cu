@@ -64,9 +64,11 @@ __host__ __device__ constexpr uint32_t tiny_pattern(int P, int i = 0)
 // Carried sieve state of one persistent CTA: off[i] = first hit of prime i in the
 // NEXT window, relative to its start (valid for primes active in this window).
 constexpr uint32_t kTileBits = 32u * kTileWords;
+constexpr uint32_t kMedMax = 1024;           // medium primes 37..kWarpPrimeMax (1017 of them)
 struct Carry {
     uint32_t *off;
     uint32_t n_carry;
+    uint32_t n_steady;       // primes [i_med, n_steady): carried, p^2 <= window start
     bool have_prev;
 };
 
@@ -131,90 +133,98 @@ __device__ void sieve_window(uint32_t *win, int64_t g0, uint32_t nw, const Sieve
             }
         }
     }
-    __syncthreads();
     const int64_t o_lo = g0 * 32;
     const int64_t o_hi = (g0 + (int64_t)nw) * 32;
     const uint32_t nbits = nw * 32;
-    const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+    const int lane = tid & 31, warp = tid >> 5;
     // With a carry context (persistent verify CTAs walking consecutive tiles) the
-    // first hit of every active prime comes from the previous tile instead of a
-    // 64-bit modulo: the window of tile t+1 starts kTileBits above that of tile t.
-    // `steady`: every sieving prime was active in the previous window too, so every
-    // carried offset is valid and < p (no p^2 checks, no modulo at all).
-    bool steady = false;
-    if (cy && cy->have_prev && sp.n_use > 0 && sp.n_use <= cy->n_carry) {
-        const uint32_t pl = __ldg(sp.primes + sp.n_use - 1);
-        steady = (int64_t)(((uint64_t)pl * pl - 3) >> 1) < o_lo - (int64_t)kTileBits;
-    }
-    // Phase M: medium primes (31 < p <= kWarpPrimeMax), one warp per prime.  Warp w
-    // takes primes i_med + w + nwarps*(32k + l); lane l computes the start offset of
-    // the k-th batch's l-th prime, then the warp marks the 32 primes one by one.
+    // first hit of a prime comes from the previous tile instead of a 64-bit modulo:
+    // the window of tile t+1 starts kTileBits above that of tile t.  Primes
+    // [i_med, n_steady) have p^2 <= the window start and were carried, so their
+    // offset is valid and < p: no p^2 check and no modulo at all ("steady").
+    const uint32_t ns = cy ? cy->n_steady : 0;
+    // Phase M setup (overlaps phase T): the first hit of every medium prime
+    // (31 < p <= kWarpPrimeMax) into shared memory, one thread per prime.
     const uint32_t m_end = sp.i_big < sp.n_use ? sp.i_big : sp.n_use;
-    for (uint32_t bi = sp.i_med + warp; bi < m_end; bi += 32u * nwarps) {
-        const uint32_t pi = bi + (uint32_t)lane * nwarps;
-        uint32_t p = 0, off = 0xFFFFFFFFu;
-        if (pi < m_end) {
-            const uint2 pt = __ldg(sp.ptm + pi);
-            p = pt.x;
-            if (steady) {
-                off = cy->off[pi];
-                cy->off[pi] = off >= pt.y ? off - pt.y : off + p - pt.y;
-            } else {
-                const int64_t opp = (int64_t)(((uint64_t)p * p - 3) >> 1);
-                if (opp < o_hi) {
-                    const bool carried = cy && pi < cy->n_carry;
-                    uint64_t o64;
-                    if (carried && cy->have_prev && opp < o_hi - (int64_t)kTileBits) o64 = cy->off[pi];
-                    else o64 = first_hit(p, __ldg(sp.magic + pi), o_lo, o_hi);
-                    off = (uint32_t)o64;
-                    if (carried) cy->off[pi] = next_tile_off(off, p, pt.y);
-                }
+    __shared__ uint32_t sh_moff[kMedMax];
+    __shared__ uint32_t sh_mnext;
+    if (tid == 0) sh_mnext = sp.i_med;
+    for (uint32_t pi = sp.i_med + tid; pi < m_end; pi += nt) {
+        const uint2 pt = __ldg(sp.ptm + pi);
+        const uint32_t p = pt.x;
+        uint32_t off = 0xFFFFFFFFu;
+        if (pi < ns) {
+            off = cy->off[pi];
+            cy->off[pi] = off >= pt.y ? off - pt.y : off + p - pt.y;
+        } else {
+            const int64_t opp = (int64_t)(((uint64_t)p * p - 3) >> 1);
+            if (opp < o_hi) {
+                const bool carried = cy && pi < cy->n_carry;
+                uint64_t o64;
+                if (carried && cy->have_prev && opp < o_hi - (int64_t)kTileBits) o64 = cy->off[pi];
+                else o64 = first_hit(p, __ldg(sp.magic + pi), o_lo, o_hi);
+                off = (uint32_t)o64;
+                if (carried) cy->off[pi] = next_tile_off(off, p, pt.y);
             }
         }
-        const uint32_t n_here = min(32u, (m_end - bi + nwarps - 1) / nwarps);
-        for (uint32_t i = 0; i < n_here; ++i) {
-            const uint32_t pp = __shfl_sync(FULL, p, i);
-            const uint32_t oo = __shfl_sync(FULL, off, i);
-            if (oo >= nbits) continue;
-            const uint32_t stride = 32 * pp;
-            for (uint32_t b = oo + lane * pp; b < nbits; b += stride)
-                atomicAnd(win + (b >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b));   // ~(1 << b%32)
-        }
+        sh_moff[pi - sp.i_med] = off;
     }
-    // Phase B: large primes, one thread per prime (next prime's loads issued early).
+    __syncthreads();
+    // Phase M: one warp per medium prime, primes handed out dynamically in
+    // ascending order (largest work first), so the warps finish together.
+    while (true) {
+        uint32_t pi = 0;
+        if (lane == 0) pi = atomicAdd(&sh_mnext, 1u);
+        pi = __shfl_sync(FULL, pi, 0);
+        if (pi >= m_end) break;
+        const uint32_t off = sh_moff[pi - sp.i_med];
+        if (off >= nbits) continue;
+        const uint32_t p = __ldg(sp.primes + pi);
+        const uint32_t stride = 32 * p;
+        for (uint32_t b = off + lane * p; b < nbits; b += stride)
+            atomicAnd(win + (b >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b));   // ~(1 << b%32)
+    }
+    // Phase B: large primes, one thread per prime.  Steady primes first (the next
+    // prime's loads issued before this prime's marks), then the rest.
     const uint32_t b_begin = sp.i_big > sp.i_med ? sp.i_big : sp.i_med;
-    if (steady) {
-        uint32_t pi = b_begin + tid;
-        uint2 pt = make_uint2(0, 0);
-        uint32_t off = 0;
-        if (pi < sp.n_use) { pt = __ldg(sp.ptm + pi); off = cy->off[pi]; }
-        for (; pi < sp.n_use; pi += nt) {
-            const uint32_t pn = pi + nt;
-            uint2 ptn = make_uint2(0, 0);
-            uint32_t offn = 0;
-            if (pn < sp.n_use) { ptn = __ldg(sp.ptm + pn); offn = cy->off[pn]; }
-            const uint32_t p = pt.x;
-            for (uint32_t b = off; b < nbits; b += p)
-                atomicAnd(win + (b >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b));
-            cy->off[pi] = off >= pt.y ? off - pt.y : off + p - pt.y;
-            pt = ptn;
-            off = offn;
+    const uint32_t s_end = ns > b_begin ? (ns < sp.n_use ? ns : sp.n_use) : b_begin;
+    // steady: kB primes per thread in flight (their loads issued together) to hide
+    // the L2 latency of the per-CTA carry rows
+    constexpr int kB = 8;
+    // warp-uniform trip count (so __syncwarp below is legal)
+    for (uint32_t w0 = b_begin + (tid & ~31u); w0 < s_end; w0 += kB * nt) {
+        const uint32_t p0 = w0 + lane;
+        uint2 pt[kB];
+        uint32_t off[kB];
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+            const uint32_t pi = p0 + k * nt;
+            if (pi < s_end) { pt[k] = __ldg(sp.ptm + pi); off[k] = cy->off[pi]; }
+            else { pt[k] = make_uint2(1, 0); off[k] = nbits; }
         }
-    } else {
-        for (uint32_t pi = b_begin + tid; pi < sp.n_use; pi += nt) {
-            const uint2 pt = __ldg(sp.ptm + pi);
-            const uint32_t p = pt.x;
-            const int64_t opp = (int64_t)(((uint64_t)p * p - 3) >> 1);
-            if (opp >= o_hi) break;
-            const bool carried = cy && pi < cy->n_carry;
-            uint64_t off;
-            if (carried && cy->have_prev && opp < o_hi - (int64_t)kTileBits) off = cy->off[pi];
-            else off = first_hit(p, __ldg(sp.magic + pi), o_lo, o_hi);
-            uint32_t b = (uint32_t)min(off, (uint64_t)nbits);
-            for (; b < nbits; b += p)
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+            const uint32_t p = pt[k].x;
+            for (uint32_t b = off[k]; b < nbits; b += p)
                 atomicAnd(win + (b >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b));
-            if (carried) cy->off[pi] = next_tile_off((uint32_t)off, p, pt.y);
+            const uint32_t pi = p0 + k * nt;
+            if (pi < s_end) cy->off[pi] = off[k] >= pt[k].y ? off[k] - pt[k].y : off[k] + p - pt[k].y;
         }
+        __syncwarp();   // reconverge: the per-lane hit loops diverge
+    }
+    for (uint32_t pi = s_end + tid; pi < sp.n_use; pi += nt) {
+        const uint2 pt = __ldg(sp.ptm + pi);
+        const uint32_t p = pt.x;
+        const int64_t opp = (int64_t)(((uint64_t)p * p - 3) >> 1);
+        if (opp >= o_hi) break;
+        const bool carried = cy && pi < cy->n_carry;
+        uint64_t off;
+        if (carried && cy->have_prev && opp < o_hi - (int64_t)kTileBits) off = cy->off[pi];
+        else off = first_hit(p, __ldg(sp.magic + pi), o_lo, o_hi);
+        uint32_t b = (uint32_t)min(off, (uint64_t)nbits);
+        for (; b < nbits; b += p)
+            atomicAnd(win + (b >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b));
+        if (carried) cy->off[pi] = next_tile_off((uint32_t)off, p, pt.y);
     }
 }
 
@@ -706,12 +716,45 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
     cy.off = a.carry ? a.carry + (uint64_t)blockIdx.x * a.carry_stride : nullptr;
     cy.n_carry = a.carry ? a.n_carry : 0;
     cy.have_prev = false;
+    cy.n_steady = 0;
+    __shared__ uint32_t sh_ns;
+    uint32_t ns_run = 0;                       // thread 0: running count (monotone in the tile)
 
     for (uint64_t tile = t_begin; tile < t_end; ++tile) {
         const uint64_t u0 = a.u_first + tile * kTileWords;
         const uint32_t tw = (uint32_t)min((uint64_t)kTileWords, a.u_end - u0);
         __syncthreads();                      // previous tile fully consumed
-        if (tid == 0) sh_next = 0;
+        if (tid == 0) {
+            sh_next = 0;
+            // steady primes of this window: carried (previous tile done by this CTA)
+            // and p^2 <= 2*o_lo + 3, i.e. (p^2 - 3)/2 <= o_lo
+            uint32_t ns = 0;
+            const int64_t o_lo = ((int64_t)u0 - (int64_t)a.halo) * 32;
+            if (cy.have_prev && o_lo > 0) {
+                const uint64_t lim = 2 * (uint64_t)o_lo + 3;
+                const uint32_t top = min(cy.n_carry, a.sp.n_use);
+                ns = max(ns_run, a.sp.i_med);
+                if (ns == a.sp.i_med) {              // first use: binary search
+                    uint32_t lo = a.sp.i_med, hi = top;
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        const uint64_t pm = __ldg(a.sp.primes + mid);
+                        if (pm * pm <= lim) lo = mid + 1; else hi = mid;
+                    }
+                    ns = lo;
+                } else {
+                    while (ns < top) {
+                        const uint64_t pm = __ldg(a.sp.primes + ns);
+                        if (pm * pm > lim) break;
+                        ++ns;
+                    }
+                }
+                ns_run = ns;
+            }
+            sh_ns = ns;
+        }
+        __syncthreads();
+        cy.n_steady = sh_ns;
         sieve_window(win, (int64_t)u0 - a.halo, a.halo + tw, a.sp, a.carry ? &cy : nullptr);
         cy.have_prev = true;
         __syncthreads();
