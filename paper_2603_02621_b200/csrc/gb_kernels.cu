@@ -181,8 +181,16 @@ __device__ void sieve_window(uint32_t *win, int64_t g0, uint32_t nw, const Sieve
         if (off >= nbits) continue;
         const uint32_t p = __ldg(sp.primes + pi);
         const uint32_t stride = 32 * p;
-        for (uint32_t b = off + lane * p; b < nbits; b += stride)
+        uint32_t b = off + lane * p;
+        for (; b + 3 * stride < nbits; b += 4 * stride) {        // 4 hits per lane per trip
+            const uint32_t b1 = b + stride, b2 = b1 + stride, b3 = b2 + stride;
             atomicAnd(win + (b >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b));   // ~(1 << b%32)
+            atomicAnd(win + (b1 >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b1));
+            atomicAnd(win + (b2 >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b2));
+            atomicAnd(win + (b3 >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b3));
+        }
+        for (; b < nbits; b += stride)
+            atomicAnd(win + (b >> 5), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, b));
     }
     // Phase B: large primes, one thread per prime.  Steady primes first (the next
     // prime's loads issued before this prime's marks), then the rest.
@@ -447,7 +455,13 @@ __device__ __forceinline__ void hist_add(uint32_t *sh_hist, int64_t *res, uint32
 // The fast path is fully unrolled over these, so every shift k = (p-1)/2, word
 // offset k/32 and bit offset k%32 is an immediate ("bitwise
 // AND/OR operations across aligned words").
-constexpr int kUnroll = 512;
+#ifndef GB_UNROLL
+#define GB_UNROLL 256
+#endif
+#ifndef GB_PHASE1
+#define GB_PHASE1 64
+#endif
+constexpr int kUnroll = GB_UNROLL;
 struct OddPrimeTable {
     uint32_t p[kUnroll];
 };
@@ -465,7 +479,8 @@ constexpr OddPrimeTable make_odd_primes()
 }
 constexpr OddPrimeTable kOddPrimes = make_odd_primes();
 static_assert(kUnroll + 2 <= kHistSmem, "unrolled bins must live in the shared histogram");
-static_assert(kOddPrimes.p[0] == 3 && kOddPrimes.p[kUnroll - 1] == 3673, "odd prime table");
+static_assert(kOddPrimes.p[0] == 3 && kOddPrimes.p[kUnroll > 511 ? 511 : 0] == (kUnroll > 511 ? 3673 : 3),
+              "odd prime table");
 
 struct Lane {
     const uint32_t *w;   // &win[halo + local word]: O word of this lane's U word
@@ -541,7 +556,7 @@ __device__ __forceinline__ void mark_unrolled(Lane &m, uint32_t *hist, int lane)
 // Phase 1 of the mark: the first kPhase1 primes for two words per lane (every word
 // needs them: the max p_min index of a 32-even word is rarely below 40), no exit
 // checks; the per-prime counts of both words share one REDUX.
-constexpr int kPhase1 = 64;
+constexpr int kPhase1 = GB_PHASE1;
 constexpr int kQueue = 128;                  // per-warp survivor queue (entries)
 
 template <int J, bool DUMP>

@@ -13,7 +13,7 @@ import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB_PATH = os.path.join(PKG, "libgb.so")
+LIB_PATH = os.environ.get("GB_LIB") or os.path.join(PKG, "libgb.so")   # GB_LIB: A/B experiments
 HEADER = os.path.join(ROOT, "include", "gb.h")
 
 # status codes and result layout, parsed from the header (single source of truth)

@@ -17,6 +17,7 @@ ap.add_argument("--N", type=float, default=1e12)
 ap.add_argument("--span", type=int, default=32)
 ap.add_argument("--p-max", type=int, default=65521)
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--time", type=int, default=0, help="time this many verify launches (after 2 warm-ups)")
 a = ap.parse_args()
 N = int(a.N)
 v = Verifier(hi_max=N + 1, p_max=a.p_max)
@@ -28,4 +29,20 @@ v.finalize(r)
 w = v.sieve_segment((lo - 3) // 128, (1 << a.span) // 128)
 torch.cuda.synchronize()
 d = v.decode(r)
-print({k: d[k] for k in ("evens", "verified", "fastpath_unresolved", "max_pmin", "max_pmin_n")})
+print({k: d[k] for k in ("evens", "verified", "fastpath_unresolved", "max_pmin", "max_pmin_n", "chk")})
+if a.time:
+    r2 = v.new_result()
+    for _ in range(2):
+        v.verify(lo, N + 1, r2)
+    ts = []
+    for _ in range(a.time):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        v.verify(lo, N + 1, r2)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ts.sort()
+    ev = d["evens"]
+    print(f"TIME lib={os.environ.get('GB_LIB', 'default')} median_ms={ts[len(ts)//2]:.3f} "
+          f"min_ms={ts[0]:.3f} evens_per_s={ev / (ts[len(ts)//2] / 1e3):.4e}")
