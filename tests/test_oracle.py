@@ -221,3 +221,34 @@ def test_cap_and_pfast_semantics():
     first = 4 + 2 * int(np.flatnonzero(d > 5)[0])
     assert rc["first_unresolved_n"] == first == 30          # p_min(30) = 7
     assert rc["hist"][0] == rc["unresolved"]
+
+
+@pytest.mark.parametrize("N,tag", [("1000000000", "1e09"), ("10000000000", "1e10"),
+                                   ("100000000000", "1e11")])
+def test_golden_files_match_appendix(N, tag):
+    """The oracle-written golden JSONs agree with SURVEY Appendix A (computed by an
+    independent throwaway program) and with published pi / pi2."""
+    path = os.path.join(GOLDEN, f"verify_{tag}.json")
+    if not os.path.exists(path):
+        pytest.skip("golden not generated")
+    g = json.load(open(path))["result"]
+    a = AGG[N]
+    assert g["evens"] == a["evens"] and g["sum_pmin"] == a["sum_pmin"]
+    assert (g["max_pmin"], g["max_pmin_n"]) == (a["max_pmin"], a["max_pmin_n"])
+    idx = prime_index_bins(100)
+    for p, c in a["hist_by_p"].items():
+        assert g["hist"][str(idx[int(p)])] == c
+    assert g["hist"]["2"] == PUB["pi"][N] - 1
+    assert g["hist"]["3"] == PUB["pi"][N] - 1 - PUB["pi2"][N]
+
+
+def test_golden_1e12_closed_forms():
+    """1e12 golden (oracle only) vs published pi(1e12), pi2(1e12)."""
+    path = os.path.join(GOLDEN, "verify_1e12.json")
+    if not os.path.exists(path):
+        pytest.skip("golden not generated")
+    g = json.load(open(path))["result"]
+    assert g["evens"] == 10**12 // 2 - 1
+    assert g["hist"]["2"] == PUB["pi"]["1000000000000"] - 1 == 37607912017
+    assert g["hist"]["3"] == PUB["pi"]["1000000000000"] - 1 - PUB["pi2"]["1000000000000"] == 35737326797
+    assert g["unresolved"] == 0 and g["fastpath_unresolved"] == 0
