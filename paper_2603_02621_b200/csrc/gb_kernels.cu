@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdio>
 
 #include "gb_internal.h"
 #include "mr64.cuh"
@@ -29,6 +30,9 @@ extern "C" uint64_t gb_launch_count(void) { return gb::g_launches.load(); }
 namespace gb {
 
 constexpr uint32_t FULL = 0xffffffffu;
+#ifdef GB_PROFILE_PHASES
+__device__ unsigned long long g_prof[4];
+#endif
 
 // ---------------------------------------------------------------------------
 // small helpers
@@ -739,6 +743,9 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
         const uint64_t u0 = a.u_first + tile * kTileWords;
         const uint32_t tw = (uint32_t)min((uint64_t)kTileWords, a.u_end - u0);
         __syncthreads();                      // previous tile fully consumed
+#ifdef GB_PROFILE_PHASES
+        long long t_start = clock64();
+#endif
         if (tid == 0) {
             sh_next = 0;
             // steady primes of this window: carried (previous tile done by this CTA)
@@ -773,6 +780,9 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
         sieve_window(win, (int64_t)u0 - a.halo, a.halo + tw, a.sp, a.carry ? &cy : nullptr);
         cy.have_prev = true;
         __syncthreads();
+#ifdef GB_PROFILE_PHASES
+        long long t_sieved = clock64();
+#endif
 
         if constexpr (UNROLL) {
             // phase 1: rounds of 64 words (2 per lane) through the first kPhase1 primes,
@@ -855,7 +865,22 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
             }
         }
         // per-tile flush of the shared histogram keeps its 32-bit bins exact
+#ifdef GB_PROFILE_PHASES
+        long long t_marked = clock64();
+#endif
         __syncthreads();
+#ifdef GB_PROFILE_PHASES
+        long long t_synced = clock64();
+        if (lane == 0) {
+            atomicAdd(&g_prof[0], (unsigned long long)(t_sieved - t_start));
+            atomicAdd(&g_prof[1], (unsigned long long)(t_marked - t_sieved));
+            atomicAdd(&g_prof[2], (unsigned long long)(t_synced - t_marked));
+            atomicAdd(&g_prof[3], 1ull);
+        }
+        if (blockIdx.x == 0 && tid == 0 && tile + 1 == t_end)
+            printf("GBPROF sieve=%llu mark=%llu markwait=%llu warp-tiles=%llu (cycles summed over warps, all CTAs so far)\n",
+                   g_prof[0], g_prof[1], g_prof[2], g_prof[3]);
+#endif
         {
             unsigned long long *R = (unsigned long long *)a.result;
             for (int i = tid; i < kHistSmem; i += blockDim.x) {
