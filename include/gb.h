@@ -65,7 +65,7 @@ typedef struct gb_ctx gb_ctx;   /* opaque; host object owned by libgb */
 #define GB_R_MAX_KEY              9   /* MAX: (p_min << 40) | (2^40-1 - (n-origin)/2);
                                          largest p_min, ties to the smallest n       */
 #define GB_R_CHK_RAW             10   /* device accumulator of CHK = sum of
-                                         p_min(n) * floor((n-4)/64) mod 2^64; moved
+                                         p_min(n) * floor(n/192) mod 2^64; moved
                                          into LO32/HI32 and zeroed by finalize       */
 #define GB_R_HIST                16   /* SUM: hist[0..GB_NBINS)                       */
 #define GB_NBINS               6544   /* hist[0] = unresolved; hist[i] = #n with p_min

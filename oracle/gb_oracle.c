@@ -35,7 +35,9 @@
  *   R5 aggregates: histogram of p_min by prime index (bin 0 = unresolved,
  *      bin i = i-th prime, p_1 = 2, ..., p_6542 = 65521, bin 6543 = larger),
  *      max p_min with the SMALLEST n attaining it (A025018 convention),
- *      sum of p_min, and chk = sum of p_min(n) * floor((n - 4) / 64) mod 2^64.
+ *      sum of p_min, and chk = sum of p_min(n) * floor(n / 192) mod 2^64
+ *      (reading R6: a checksum sensitive to which 192-integer block
+ *      each p_min lands in; the paper defines none).
  *
  * Build: gcc -O2 -std=c11 -pthread -shared -fPIC gb_oracle.c -o liboracle.so
  */
@@ -58,7 +60,7 @@ typedef struct {
     int64_t max_pmin;            /* 0 if no verified n */
     int64_t max_pmin_n;          /* smallest n with p_min == max_pmin */
     int64_t sum_pmin;
-    uint64_t chk;                /* sum p_min(n) * floor((n-4)/64)  mod 2^64 */
+    uint64_t chk;                /* sum p_min(n) * floor(n/192)  mod 2^64 */
     int64_t hist[OR_NBINS];
 } or_result;
 
@@ -202,7 +204,7 @@ static void record(worker *w, uint64_t n, uint64_t p)
     if (p > w->p_fast) r->fastpath_unresolved++;
     r->hist[bin_of(w->sp, p)]++;
     r->sum_pmin += (int64_t)p;
-    r->chk += (uint64_t)p * ((n - 4) / 64);
+    r->chk += (uint64_t)p * (n / 192);
     if ((int64_t)p > r->max_pmin || ((int64_t)p == r->max_pmin && (int64_t)n < r->max_pmin_n)) {
         r->max_pmin = (int64_t)p;
         r->max_pmin_n = (int64_t)n;

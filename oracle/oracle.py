@@ -33,8 +33,10 @@ class OrResult(ctypes.Structure):
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (the checker is built, not used, by build())."""
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        tmp = f"{LIB}.{os.getpid()}.tmp"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-pthread", "-shared",
-                               "-fPIC", SRC, "-o", LIB])
+                               "-fPIC", SRC, "-o", tmp])
+        os.replace(tmp, LIB)      # new inode: never rewrite a library a running process maps
     return LIB
 
 

@@ -11,8 +11,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libgb.so")
-SOURCES = ["gb_kernels.cu", "gb_api.cu"]
-HEADERS = ["gb_internal.h", "mr64.cuh"]
+SOURCES = ["gb_kernels.cu", "gb_verify.cu", "gb_api.cu"]
+HEADERS = ["gb_internal.h", "mr64.cuh", "gb_device.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -62,8 +62,8 @@ bool plan(uint64_t hi_max, uint32_t p_max, Layout &L)
     L.off_bits = o;    o = align_up(o + 8 * L.bits_words, 256);
     L.off_primes = o;  o = align_up(o + 4 * L.list_cap, 256);
     L.off_magic = o;   o = align_up(o + 8 * L.list_cap, 256);
-    L.off_tmod = o;    o = align_up(o + 8 * L.list_cap, 256);
-    L.off_carry = o;   o = align_up(o + 4 * L.carry_stride * (uint64_t)kMaxBlocksPerSm * kMaxSms, 256);
+    L.off_tmod = o;    o = align_up(o + 16 * L.list_cap, 256);
+    L.off_carry = o;   o = align_up(o + 8 * L.carry_stride * (uint64_t)kMaxBlocksPerSm * kMaxSms, 256);
     L.off_blk = o;     o = align_up(o + 8 * (L.n_blk + 1), 256);
     L.off_counter = o; o = align_up(o + 256, 256);
     L.off_res = o;     o = align_up(o + 8 * (uint64_t)GB_RESULT_WORDS, 256);
@@ -81,12 +81,16 @@ uint32_t count_le(const std::vector<uint32_t> &v, uint64_t x)
     return (uint32_t)(std::upper_bound(v.begin(), v.end(), (uint32_t)x) - v.begin());
 }
 
+// wheel halo: the largest shift of a candidate p is p/6 + 1 bits
+uint32_t verify_halo(uint32_t p_top) { return ((p_top / 6 + 1) >> 5) + 1; }
+size_t verify_smem(uint32_t halo) { return 2 * 4ull * (halo + kTileWords); }
+
 SievePrimes sieve_primes(const gb_ctx *c, uint64_t sqrt_bound)
 {
     SievePrimes sp;
     sp.primes = c->primes;
     sp.magic = c->magic;
-    sp.ptm = c->ptm;
+    sp.pk = c->pk;
     sp.i_med = count_le(c->h_primes, 31);
     sp.i_big = count_le(c->h_primes, kWarpPrimeMax);
     sp.n_use = count_le(c->h_primes, sqrt_bound);
@@ -153,7 +157,7 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
     c->bits_words = L.bits_words;
     c->primes = (uint32_t *)(ws + L.off_primes);
     c->magic = (uint64_t *)(ws + L.off_magic);
-    c->ptm = (uint2 *)(ws + L.off_tmod);
+    c->pk = (uint4 *)(ws + L.off_tmod);
     c->carry = (uint32_t *)(ws + L.off_carry);
     c->carry_stride = L.carry_stride;
     c->blk = (uint64_t *)(ws + L.off_blk);
@@ -169,7 +173,7 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
     cudaStream_t st = S(stream);
     // K-BASE stage 1: seed primes <= isqrt(R) (with per-prime magic)
     const uint64_t s = isqrt_u64(L.R);
-    if (launch_seed(s, c->primes, c->magic, c->ptm, c->counter, st) != cudaSuccess) { delete c; return GB_ECUDA; }
+    if (launch_seed(s, c->primes, c->magic, c->pk, c->counter, st) != cudaSuccess) { delete c; return GB_ECUDA; }
     uint32_t n_seed = 0;
     if (cudaMemcpyAsync(&n_seed, c->counter, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess) {
@@ -192,7 +196,7 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
     // K-BASE stage 3: compaction into the ascending list (+ magic)
     if (launch_count_bits(c->bits, L.bits_words, c->blk, st) != cudaSuccess ||
         launch_scan(c->blk, L.n_blk, st) != cudaSuccess ||
-        launch_scatter(c->bits, L.bits_words, c->blk, c->primes, c->magic, c->ptm, st) != cudaSuccess) {
+        launch_scatter(c->bits, L.bits_words, c->blk, c->primes, c->magic, c->pk, st) != cudaSuccess) {
         delete c;
         return GB_ECUDA;
     }
@@ -211,8 +215,7 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
     }
     // verify kernel smem limit for the largest p_max this ctx accepts
     const uint32_t n_cand = count_le(c->h_primes, p_max);
-    const uint32_t kmax = (c->h_primes[n_cand - 1] - 1) / 2;
-    const size_t smem_max = 4ull * ((kmax >> 5) + 1 + kTileWords);
+    const size_t smem_max = verify_smem(verify_halo(c->h_primes[n_cand - 1]));
     if (configure_verify(smem_max) != cudaSuccess) { delete c; return GB_ECUDA; }
     *out = c;
     return GB_OK;
@@ -280,20 +283,31 @@ gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_m
     if (hi <= lo_e) return GB_OK;                            // empty range: no launch
     if (hi > ctx->hi_max) return GB_ERANGE;
     if (lo_e < ctx->origin || ((hi - ctx->origin) >> 1) >= (1ull << GB_KEY_SHIFT)) return GB_EINVAL;
-    const uint64_t n_last = (hi - 1) & ~1ull;                // largest even n < hi
     VerifyArgs a;
-    a.e_lo = (lo_e - 4) / 2;
-    a.e_hi = (n_last - 4) / 2 + 1;
+    // wheel classes n = 6m + c (c = 0, 2, 4): valid m in [ceil((lo_e-c)/6), ceil((hi-c)/6))
+    uint64_t mlo_min = UINT64_MAX, mhi_max = 0;
+    for (int k = 0; k < 3; ++k) {
+        const uint64_t c = 2 * (uint64_t)k;
+        a.m_lo[k] = (lo_e - c + 5) / 6;
+        a.m_hi[k] = (hi - c + 5) / 6;
+        if (a.m_lo[k] < a.m_hi[k]) {
+            mlo_min = std::min(mlo_min, a.m_lo[k]);
+            mhi_max = std::max(mhi_max, a.m_hi[k]);
+        }
+    }
+    if (mhi_max == 0) return GB_OK;                          // no even n in range
     const uint64_t r = isqrt_u64(hi - 1);
     if (r > ctx->R) return GB_ERANGE;
     a.sp = sieve_primes(ctx, r);
+    if (a.sp.i_big - a.sp.i_med > 1024) return GB_EINTERNAL;
     a.n_cand = count_le(ctx->h_primes, p_max);
     if (a.n_cand == 0) return GB_EINVAL;
     const uint32_t p_top = ctx->h_primes[a.n_cand - 1];
-    a.halo = (((p_top - 1) / 2) >> 5) + 1;
-    a.u_first = a.e_lo >> 5;
-    a.u_end = ((a.e_hi - 1) >> 5) + 1;
+    a.halo = verify_halo(p_top);
+    a.u_first = mlo_min >> 5;
+    a.u_end = ((mhi_max - 1) >> 5) + 1;
     a.n_tiles = (a.u_end - a.u_first + kTileWords - 1) / kTileWords;
+    a.lo_e = lo_e;
     a.origin = ctx->origin;
     a.p_fallback = (uint64_t)p_top + 2;
     a.cap = fallback_p_cap;
@@ -303,7 +317,7 @@ gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_m
     a.result = d_result;
     a.dump = d_pmin_dump;
     DeviceGuard g(ctx->device);
-    const size_t smem = 4ull * (a.halo + kTileWords);
+    const size_t smem = verify_smem(a.halo);
     const int per_sm = verify_blocks_per_sm(smem);
     const uint64_t max_grid = (uint64_t)per_sm * ctx->num_sms;
     const int grid = (int)std::min<uint64_t>(std::min<uint64_t>(a.n_tiles, max_grid), ctx->carry_ctas);

@@ -12,7 +12,8 @@ namespace gb {
 
 // ---- tiling constants (tuned for sm_100a: 148 SMs, 228 KB smem / SM) ----
 constexpr int kThreads = 512;              // threads per CTA, every kernel
-constexpr int kTileWords = 16384;          // 32-bit U words per verify tile = 524288 evens
+constexpr int kTileWords = 8192;           // verify tile: 32-bit words per mod-6 class
+constexpr uint32_t kTileM = 32u * kTileWords;  // m-span of a tile (n = 6m + a): 786432 evens
 constexpr int kSieveTileWords = 16384;     // 32-bit words per gb_sieve_segment CTA
 constexpr int kHistSmem = 1024;            // histogram bins kept in shared memory
 constexpr uint32_t kWarpPrimeMax = 8192;   // primes <= this: one warp per prime
@@ -26,7 +27,7 @@ constexpr int kMaxBlocksPerSm = 4;         // sizing bound for per-CTA carry sto
 struct SievePrimes {
     const uint32_t *primes;   // odd primes ascending (3, 5, 7, ...)
     const uint64_t *magic;    // floor((2^64-1)/p) per prime
-    const uint2 *ptm;         // (p, (32*kTileWords) mod p) per prime
+    const uint4 *pk;          // (p, kTileM mod p, rA, rB) per prime (see make_pk)
     uint32_t i_med;           // first index with p > 31 (word patterns below)
     uint32_t i_big;           // first index with p > kWarpPrimeMax
     uint32_t n_use;           // primes usable (p^2 beyond the window are skipped)
@@ -40,14 +41,17 @@ struct SegmentArgs {
     uint32_t *out;            // n_words32 words
 };
 
+// The fused verify kernel works on the mod-6 wheel (gb_verify.cu): even n = 6m + a
+// (classes a = 0, 2, 4) and odd q = 6m + 1 (class A) / 6m + 5 (class B).
 struct VerifyArgs {
     SievePrimes sp;
     uint32_t n_cand;          // odd primes p <= p_max used by the fast path
-    uint32_t halo;            // H32 = ((p_cand_max-1)/2 >> 5) + 1 words below a tile
-    uint64_t e_lo, e_hi;      // even-index range [e_lo, e_hi), e(n) = (n-4)/2
-    uint64_t u_first;         // first 32-bit U word
-    uint64_t u_end;           // one past the last U word
+    uint32_t halo;            // words per class below a tile: (max shift >> 5) + 1
+    uint64_t m_lo[3], m_hi[3];  // class a = 0, 2, 4: valid m in [m_lo, m_hi)
+    uint64_t u_first;         // first 32-bit word (u = m >> 5, same for all classes)
+    uint64_t u_end;           // one past the last word
     uint64_t n_tiles;
+    uint64_t lo_e;            // dump index = (n - lo_e) / 2
     uint64_t origin;          // MAX_KEY origin
     uint64_t p_fallback;      // first odd candidate after the fast path (p_cand_max + 2)
     uint64_t cap;             // fallback p cap (test hook)
@@ -56,20 +60,20 @@ struct VerifyArgs {
     uint32_t n_base;          // odd primes in the resident list
     int64_t *result;
     uint32_t *dump;           // nullable
-    uint32_t *carry;          // per-CTA carried sieve offsets (nullable)
-    uint64_t carry_stride;    // u32 entries per CTA
+    uint32_t *carry;          // per-CTA carried sieve offsets, 2 per prime (nullable)
+    uint64_t carry_stride;    // u32 entries per class per CTA (row = 2 * carry_stride)
     uint32_t n_carry;         // primes [0, n_carry) carried
 };
 
 // Launchers (gb_kernels.cu).  Each returns the cudaGetLastError() of its launch.
-cudaError_t launch_seed(uint64_t s, uint32_t *primes, uint64_t *magic, uint2 *ptm,
+cudaError_t launch_seed(uint64_t s, uint32_t *primes, uint64_t *magic, uint4 *pk,
                         uint32_t *d_count, cudaStream_t st);
 cudaError_t launch_segment(const SegmentArgs &a, cudaStream_t st);
 cudaError_t launch_count_bits(const uint64_t *bits, uint64_t n_words, uint64_t *blk,
                               cudaStream_t st);
 cudaError_t launch_scan(uint64_t *blk, uint64_t n_blk, cudaStream_t st);
 cudaError_t launch_scatter(const uint64_t *bits, uint64_t n_words, const uint64_t *blk,
-                           uint32_t *primes, uint64_t *magic, uint2 *ptm, cudaStream_t st);
+                           uint32_t *primes, uint64_t *magic, uint4 *pk, cudaStream_t st);
 cudaError_t launch_result_init(int64_t *res, cudaStream_t st);
 cudaError_t launch_result_finalize(int64_t *res, cudaStream_t st);
 cudaError_t launch_verify(const VerifyArgs &a, int grid, size_t smem, cudaStream_t st);
@@ -77,6 +81,7 @@ cudaError_t launch_is_prime(const uint64_t *x, uint8_t *out, uint64_t n, const u
                             uint64_t R, cudaStream_t st);
 cudaError_t configure_verify(size_t smem_max);
 int verify_blocks_per_sm(size_t smem);
+uint32_t unroll_p_max();       // largest prime of the unrolled class tables
 
 void count_launch();
 
@@ -93,7 +98,7 @@ struct gb_ctx {
     uint64_t bits_words;
     uint32_t *primes;      // odd primes <= R
     uint64_t *magic;
-    uint2 *ptm;            // (p, (32*kTileWords) mod p)
+    uint4 *pk;             // (p, kTileM mod p, rA, rB)
     uint32_t *carry;       // verify-kernel carried offsets: carry_ctas x carry_stride
     uint64_t carry_stride;
     uint32_t carry_ctas;

@@ -1,0 +1,828 @@
+// gb_verify.cu -- K-VERIFY: the fused segment sieve -> inverted bulk marking ->
+// exhaustive fallback, on the mod-6 wheel.
+//
+// The method (section 2.3.1): "iterate over candidate primes p and
+// mark all even n for which q = n - p is prime", in the bitwise bulk-marking form
+// of PAPER.md:406-410 ("replacing per-n lookups with bitwise AND/OR operations
+// across aligned words"), with the segment sieve on the GPU.
+//
+// Wheel layout (a B200 design choice; results are the plain definition's):
+//   even n = 6m + a, a in {0, 2, 4}     -> U classes U0, U2, U4 (bit m of class a)
+//   odd  q = 6m + 1 (class A), 6m + 5 (class B); q divisible by 3 is never prime
+//   except 3 itself, so the sieve keeps 1 bit per 3 integers instead of 1 per 2.
+// For p = 6j + b the partner q = n - p is:
+//   a = 0: b = 1 -> B[m - j - 1]   b = 5 -> A[m - j - 1]   (p = 3 only for n = 6)
+//   a = 2: b = 1 -> A[m - j]       b = 5 -> q = 0 mod 3     p = 3 -> B[m - 1]
+//   a = 4: b = 1 -> q = 0 mod 3    b = 5 -> B[m - j - 1]    p = 3 -> A[m]
+// so U2 only needs p = 3 and p = 1 (mod 6), U4 p = 3 and p = 5 (mod 6): skipping the
+// primes that can only give q = 3 (whose n then has p_min = 3 anyway) halves the
+// candidate list of two thirds of the evens.  "n - p prime" over a U word is the
+// class A or B window shifted up by s = j (+1) bits: funnelshift(O[w-a-1], O[w-a], b)
+// with s = 32a + b.
+#include <stdint.h>
+
+#include <cstdio>
+
+#include "gb_device.cuh"
+
+namespace gb {
+
+// ---------------------------------------------------------------------------
+// transitions and compile-time class tables
+// ---------------------------------------------------------------------------
+struct Trans {
+    int ok;           // 0: p never gives an odd prime partner > 3 for this class
+    int src;          // 0 = class A window, 1 = class B window
+    uint32_t shift;   // U bit m <-> src bit m - shift
+};
+
+__host__ __device__ constexpr Trans trans(int a, uint32_t p)
+{
+    if (p == 3) return a == 2 ? Trans{1, 1, 1} : (a == 4 ? Trans{1, 0, 0} : Trans{0, 0, 0});
+    const uint32_t j = p / 6, b = p % 6;
+    if (a == 0) return b == 1 ? Trans{1, 1, j + 1} : Trans{1, 0, j + 1};
+    if (a == 2) return b == 1 ? Trans{1, 0, j} : Trans{0, 0, 0};
+    return b == 5 ? Trans{1, 1, j + 1} : Trans{0, 0, 0};
+}
+
+#ifndef GB_K6
+#define GB_K6 96
+#endif
+#ifndef GB_P1
+#define GB_P1 32
+#endif
+constexpr int kK = GB_K6;        // unrolled candidates per class
+constexpr int kP1 = GB_P1;       // phase 1: candidates every word goes through
+constexpr int kQueue = 128;      // per-warp survivor queue
+static_assert(kK % 8 == 0 && kP1 % 8 == 0 && kP1 <= kK, "blocks of 8 candidates");
+
+struct ClassTable {
+    uint32_t p[kK];
+    uint32_t bin[kK];     // histogram bin = number of primes <= p (bin 1 = the prime 2)
+};
+
+__host__ __device__ constexpr bool is_prime_small(uint32_t x)
+{
+    if (x < 2) return false;
+    if (x % 2 == 0) return x == 2;
+    for (uint32_t d = 3; d * d <= x; d += 2)
+        if (x % d == 0) return false;
+    return true;
+}
+
+constexpr ClassTable make_class_table(int a)
+{
+    ClassTable t{};
+    int c = 0;
+    uint32_t nprimes = 1;   // the prime 2
+    for (uint32_t x = 3; c < kK; x += 2) {
+        if (!is_prime_small(x)) continue;
+        ++nprimes;
+        if (trans(a, x).ok) {
+            t.p[c] = x;
+            t.bin[c] = nprimes;
+            ++c;
+        }
+    }
+    return t;
+}
+
+constexpr ClassTable kTab[3] = {make_class_table(0), make_class_table(2), make_class_table(4)};
+static_assert(kTab[0].p[0] == 5 && kTab[1].p[0] == 3 && kTab[1].p[1] == 7 && kTab[2].p[1] == 5,
+              "class tables");
+static_assert(kTab[0].bin[0] == 3 && kTab[1].bin[0] == 2, "bins: 2 -> 1, 3 -> 2, 5 -> 3");
+__constant__ ClassTable c_tab[3] = {make_class_table(0), make_class_table(2), make_class_table(4)};
+
+constexpr uint32_t max3(uint32_t a, uint32_t b, uint32_t c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
+constexpr uint32_t kUnrollPMax = max3(kTab[0].p[kK - 1], kTab[1].p[kK - 1], kTab[2].p[kK - 1]);
+uint32_t unroll_p_max() { return kUnrollPMax; }
+
+// ---------------------------------------------------------------------------
+// K-SIEVE on the wheel: class A and class B windows of nw words each, word i
+// covering m in [32(g0+i), 32(g0+i)+32).  Bit = 1 iff q = 6m+1 (A) / 6m+5 (B)
+// is prime.  Multiples of p in class c are m == r_c (mod p), r_A = -1/6, r_B = -5/6.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kMedMax = 1024;
+
+struct Carry6 {
+    uint32_t *off;            // [0, stride): class A offsets, [stride, 2 stride): class B
+    uint64_t stride;
+    uint32_t n_carry;
+    uint32_t n_steady;        // primes [i_med, n_steady): carried, p^2 <= 6 m_lo + 1
+    bool have_prev;
+};
+
+__host__ __device__ constexpr uint32_t inv6(uint32_t p) { return p % 6 == 1 ? (5 * p + 1) / 6 : (p + 1) / 6; }
+__host__ __device__ constexpr uint32_t rA_of(uint32_t p) { return p - inv6(p); }
+__host__ __device__ constexpr uint32_t rB_of(uint32_t p) { return (5 * rA_of(p)) % p; }
+
+// first hit (local offset from m_lo) of the progression m == r (mod p), m >= (p^2-1)/6
+__device__ __forceinline__ uint64_t first_hit6(uint32_t p, uint32_t r, uint64_t magic, int64_t m_lo,
+                                               int64_t m_hi)
+{
+    const int64_t mmin = (int64_t)(((uint64_t)p * p - 1) / 6);
+    if (mmin >= m_hi) return UINT64_MAX;
+    const uint64_t ms = (uint64_t)(mmin > m_lo ? mmin : m_lo);
+    const uint32_t rem = mod_magic(ms, p, magic);
+    const uint32_t delta = r >= rem ? r - rem : r + p - rem;
+    return ms + delta - (uint64_t)m_lo;
+}
+
+// next tile's first hit (the window moves up by kTileM)
+__device__ __forceinline__ uint32_t next_off6(uint32_t off, uint32_t p, uint32_t tm)
+{
+    if (off >= kTileM) return off - kTileM;
+    const uint32_t om = off < p ? off : off % p;   // off >= p only when p^2 fell in this window
+    return om >= tm ? om - tm : om + p - tm;
+}
+
+__device__ __forceinline__ void mark_progression(uint32_t *w, uint32_t off, uint32_t p, uint32_t nbits,
+                                                 int lane)
+{
+    // one warp, one prime: lane l marks off + l p, off + (l + 32) p, ...
+    const uint32_t stride = 32 * p;
+    uint32_t b = off + lane * p;
+    for (; b + 3 * stride < nbits; b += 4 * stride) {
+        const uint32_t b1 = b + stride, b2 = b1 + stride, b3 = b2 + stride;
+        atomicAnd(w + (b >> 5), clear_mask(b));
+        atomicAnd(w + (b1 >> 5), clear_mask(b1));
+        atomicAnd(w + (b2 >> 5), clear_mask(b2));
+        atomicAnd(w + (b3 >> 5), clear_mask(b3));
+    }
+    for (; b < nbits; b += stride) atomicAnd(w + (b >> 5), clear_mask(b));
+}
+
+__device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
+                              Carry6 *cy)
+{
+    const int tid = threadIdx.x, lane = tid & 31;
+    constexpr int nt = kThreads;
+    // Phase T: primes 5..31 by shifted word patterns, per-thread incremental phases
+    {
+        int64_t g = g0 + tid;
+        const uint64_t gg = g < 0 ? 0 : (uint64_t)g;
+#define GB_PH(P)                                                                                   \
+    int a##P = (int)((rA_of(P) + 32u * P - (32u * (uint32_t)(gg % P)) % P) % P);                   \
+    int b##P = (int)((rB_of(P) + 32u * P - (32u * (uint32_t)(gg % P)) % P) % P);
+        GB_PH(5) GB_PH(7) GB_PH(11) GB_PH(13) GB_PH(17) GB_PH(19) GB_PH(23) GB_PH(29) GB_PH(31)
+#undef GB_PH
+        for (int64_t i = tid; i < (int64_t)nw; i += nt, g += nt) {
+            uint32_t va = 0, vb = 0;
+            if (g >= 0) {
+                const uint32_t ca = (Tiny<5>::value << a5) | (Tiny<7>::value << a7) | (Tiny<11>::value << a11) |
+                                    (Tiny<13>::value << a13) | (Tiny<17>::value << a17) |
+                                    (Tiny<19>::value << a19) | (Tiny<23>::value << a23) |
+                                    (Tiny<29>::value << a29) | (Tiny<31>::value << a31);
+                const uint32_t cb = (Tiny<5>::value << b5) | (Tiny<7>::value << b7) | (Tiny<11>::value << b11) |
+                                    (Tiny<13>::value << b13) | (Tiny<17>::value << b17) |
+                                    (Tiny<19>::value << b19) | (Tiny<23>::value << b23) |
+                                    (Tiny<29>::value << b29) | (Tiny<31>::value << b31);
+                va = ~ca;
+                vb = ~cb;
+                if (g == 0) {
+                    // restore the tiny primes themselves: A (6m+1): 7, 13, 19, 31 at m = 1, 2, 3, 5;
+                    // B (6m+5): 5, 11, 17, 23, 29 at m = 0..4; and 1 = 6*0+1 is not prime
+                    va = (va | 0x2Eu) & ~1u;
+                    vb |= 0x1Fu;
+                }
+            }
+            wA[i] = va;
+            wB[i] = vb;
+            if (g >= 0) {
+#define GB_ADV(P)                                    \
+    a##P -= (int)((32u * nt) % P); if (a##P < 0) a##P += P; \
+    b##P -= (int)((32u * nt) % P); if (b##P < 0) b##P += P;
+                GB_ADV(5) GB_ADV(7) GB_ADV(11) GB_ADV(13) GB_ADV(17) GB_ADV(19) GB_ADV(23) GB_ADV(29)
+                GB_ADV(31)
+#undef GB_ADV
+            } else if (g + nt >= 0) {
+                const uint64_t g2 = (uint64_t)(g + nt);
+#define GB_RE(P)                                                                     \
+    a##P = (int)((rA_of(P) + 32u * P - (32u * (uint32_t)(g2 % P)) % P) % P);        \
+    b##P = (int)((rB_of(P) + 32u * P - (32u * (uint32_t)(g2 % P)) % P) % P);
+                GB_RE(5) GB_RE(7) GB_RE(11) GB_RE(13) GB_RE(17) GB_RE(19) GB_RE(23) GB_RE(29) GB_RE(31)
+#undef GB_RE
+            }
+        }
+    }
+    const int64_t m_lo = g0 * 32;
+    const int64_t m_hi = (g0 + (int64_t)nw) * 32;
+    const uint32_t nbits = nw * 32;
+    const uint32_t ns = cy->n_steady;
+    // medium primes (31 < p <= kWarpPrimeMax): both first hits per prime into shared
+    // memory (carried or by modulo), one thread per prime; then one warp per prime,
+    // handed out dynamically in ascending order (largest work first).
+    const uint32_t m_end = sp.i_big < sp.n_use ? sp.i_big : sp.n_use;
+    __shared__ uint32_t sh_mA[kMedMax], sh_mB[kMedMax];
+    __shared__ uint32_t sh_mnext;
+    if (tid == 0) sh_mnext = sp.i_med;
+    for (uint32_t pi = sp.i_med + tid; pi < m_end; pi += nt) {
+        const uint4 k = __ldg(sp.pk + pi);        // p, kTileM mod p, rA, rB
+        uint32_t oa = 0xFFFFFFFFu, ob = 0xFFFFFFFFu;
+        const bool carried = pi < cy->n_carry;
+        if (pi < ns) {
+            oa = cy->off[pi];
+            ob = cy->off[cy->stride + pi];
+            cy->off[pi] = oa >= k.y ? oa - k.y : oa + k.x - k.y;
+            cy->off[cy->stride + pi] = ob >= k.y ? ob - k.y : ob + k.x - k.y;
+        } else {
+            const int64_t mmin = (int64_t)(((uint64_t)k.x * k.x - 1) / 6);
+            if (mmin < m_hi) {
+                if (carried && cy->have_prev && mmin < m_hi - (int64_t)kTileM) {
+                    oa = cy->off[pi];
+                    ob = cy->off[cy->stride + pi];
+                } else {
+                    const uint64_t mg = __ldg(sp.magic + pi);
+                    oa = (uint32_t)first_hit6(k.x, k.z, mg, m_lo, m_hi);
+                    ob = (uint32_t)first_hit6(k.x, k.w, mg, m_lo, m_hi);
+                }
+                if (carried) {
+                    cy->off[pi] = next_off6(oa, k.x, k.y);
+                    cy->off[cy->stride + pi] = next_off6(ob, k.x, k.y);
+                }
+            }
+        }
+        sh_mA[pi - sp.i_med] = oa;
+        sh_mB[pi - sp.i_med] = ob;
+    }
+    __syncthreads();
+    while (true) {
+        uint32_t pi = 0;
+        if (lane == 0) pi = atomicAdd(&sh_mnext, 1u);
+        pi = __shfl_sync(FULL, pi, 0);
+        if (pi >= m_end) break;
+        const uint32_t p = __ldg(sp.primes + pi);
+        const uint32_t oa = sh_mA[pi - sp.i_med], ob = sh_mB[pi - sp.i_med];
+        if (oa < nbits) mark_progression(wA, oa, p, nbits, lane);
+        if (ob < nbits) mark_progression(wB, ob, p, nbits, lane);
+    }
+    // large primes: one thread per prime.  Steady primes: kB in flight per thread.
+    const uint32_t b_begin = sp.i_big > sp.i_med ? sp.i_big : sp.i_med;
+    const uint32_t s_end = ns > b_begin ? (ns < sp.n_use ? ns : sp.n_use) : b_begin;
+    constexpr int kB = 4;
+    for (uint32_t w0 = b_begin + (tid & ~31u); w0 < s_end; w0 += kB * nt) {   // warp-uniform trips
+        const uint32_t p0 = w0 + lane;
+        uint2 pt[kB];
+        uint32_t oa[kB], ob[kB];
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+            const uint32_t pi = p0 + k * nt;
+            if (pi < s_end) {
+                const uint4 q = __ldg(sp.pk + pi);
+                pt[k] = make_uint2(q.x, q.y);
+                oa[k] = cy->off[pi];
+                ob[k] = cy->off[cy->stride + pi];
+            } else {
+                pt[k] = make_uint2(1, 0);
+                oa[k] = ob[k] = nbits;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+            const uint32_t p = pt[k].x, tm = pt[k].y;
+            for (uint32_t b = oa[k]; b < nbits; b += p) atomicAnd(wA + (b >> 5), clear_mask(b));
+            for (uint32_t b = ob[k]; b < nbits; b += p) atomicAnd(wB + (b >> 5), clear_mask(b));
+            const uint32_t pi = p0 + k * nt;
+            if (pi < s_end) {
+                cy->off[pi] = oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm;
+                cy->off[cy->stride + pi] = ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm;
+            }
+        }
+        __syncwarp();   // reconverge: the per-lane hit loops diverge
+    }
+    for (uint32_t pi = s_end + tid; pi < sp.n_use; pi += nt) {
+        const uint4 k = __ldg(sp.pk + pi);
+        const int64_t mmin = (int64_t)(((uint64_t)k.x * k.x - 1) / 6);
+        if (mmin >= m_hi) break;
+        const bool carried = pi < cy->n_carry;
+        uint32_t oa, ob;
+        if (carried && cy->have_prev && mmin < m_hi - (int64_t)kTileM) {
+            oa = cy->off[pi];
+            ob = cy->off[cy->stride + pi];
+        } else {
+            const uint64_t mg = __ldg(sp.magic + pi);
+            oa = (uint32_t)first_hit6(k.x, k.z, mg, m_lo, m_hi);
+            ob = (uint32_t)first_hit6(k.x, k.w, mg, m_lo, m_hi);
+        }
+        for (uint32_t b = oa; b < nbits; b += k.x) atomicAnd(wA + (b >> 5), clear_mask(b));
+        for (uint32_t b = ob; b < nbits; b += k.x) atomicAnd(wB + (b >> 5), clear_mask(b));
+        if (carried) {
+            cy->off[pi] = next_off6(oa, k.x, k.y);
+            cy->off[cy->stride + pi] = next_off6(ob, k.x, k.y);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// the inverted marking loop on one U word per lane
+// ---------------------------------------------------------------------------
+struct Lane6 {
+    const uint32_t *wa, *wb;   // class A / B window word aligned with this U word
+    uint32_t U;                // unresolved evens of the word
+    uint32_t word_sum;         // sum of p_min of bits resolved in the unrolled range
+    uint32_t lb;               // 1 + index of the last 8-candidate block with a hit (0 = none)
+    uint32_t lu;               // U at the start of that block
+    uint32_t *dump_w;          // dump entry of bit 0 (bit b at dump_w[3b]) -- DUMP only
+};
+
+template <int A, int J, bool DUMP>
+__device__ __forceinline__ uint32_t mark_step(Lane6 &m)
+{
+    constexpr uint32_t P = kTab[A / 2].p[J];
+    constexpr Trans T = trans(A, P);
+    constexpr int WA = (int)(T.shift >> 5);
+    constexpr uint32_t WB = T.shift & 31;
+    const uint32_t *src = T.src ? m.wb : m.wa;
+    const uint32_t S = __funnelshift_l(src[-(WA + 1)], src[-WA], WB);
+    const uint32_t nw = m.U & S;              // n resolved now: n - P prime, no smaller p worked
+    m.U ^= nw;
+    const uint32_t c = __popc(nw);
+    m.word_sum += c * P;
+    if constexpr (DUMP) {
+        uint32_t x = nw;
+        while (x) {
+            const int b = __ffs(x) - 1;
+            x &= x - 1;
+            m.dump_w[3 * b] = P;
+        }
+    }
+    return c;
+}
+
+// per-warp counts of 8 candidates -> class histogram (two counts per REDUX:
+// 16-bit fields, per warp and candidate <= 2048 hits)
+__device__ __forceinline__ void hist8(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t c4,
+                                      uint32_t c5, uint32_t c6, uint32_t c7, uint32_t *h, int lane)
+{
+    const uint32_t t0 = __reduce_add_sync(FULL, c0 + (c1 << 16));
+    const uint32_t t1 = __reduce_add_sync(FULL, c2 + (c3 << 16));
+    const uint32_t t2 = __reduce_add_sync(FULL, c4 + (c5 << 16));
+    const uint32_t t3 = __reduce_add_sync(FULL, c6 + (c7 << 16));
+    const uint32_t ts = (lane & 4) ? ((lane & 2) ? t3 : t2) : ((lane & 2) ? t1 : t0);
+    const uint32_t v = (lane & 1) ? (ts >> 16) : (ts & 0xffffu);
+    if (lane < 8 && v) atomicAdd(h + lane, v);
+}
+
+template <int A, int J, bool DUMP>
+__device__ __forceinline__ void block8(Lane6 &m, uint32_t *h, int lane)
+{
+    const uint32_t Ub = m.U;
+    const uint32_t c0 = mark_step<A, J + 0, DUMP>(m);
+    const uint32_t c1 = mark_step<A, J + 1, DUMP>(m);
+    const uint32_t c2 = mark_step<A, J + 2, DUMP>(m);
+    const uint32_t c3 = mark_step<A, J + 3, DUMP>(m);
+    const uint32_t c4 = mark_step<A, J + 4, DUMP>(m);
+    const uint32_t c5 = mark_step<A, J + 5, DUMP>(m);
+    const uint32_t c6 = mark_step<A, J + 6, DUMP>(m);
+    const uint32_t c7 = mark_step<A, J + 7, DUMP>(m);
+    if (m.U != Ub) { m.lb = J / 8 + 1; m.lu = Ub; }
+    hist8(c0, c1, c2, c3, c4, c5, c6, c7, h + J, lane);
+}
+
+template <int A, int J, bool DUMP>
+__device__ __forceinline__ void block8x2(Lane6 &m0, Lane6 &m1, uint32_t *h, int lane)
+{
+    const uint32_t U0 = m0.U, U1 = m1.U;
+    uint32_t c[8];
+    c[0] = mark_step<A, J + 0, DUMP>(m0); c[0] += mark_step<A, J + 0, DUMP>(m1);
+    c[1] = mark_step<A, J + 1, DUMP>(m0); c[1] += mark_step<A, J + 1, DUMP>(m1);
+    c[2] = mark_step<A, J + 2, DUMP>(m0); c[2] += mark_step<A, J + 2, DUMP>(m1);
+    c[3] = mark_step<A, J + 3, DUMP>(m0); c[3] += mark_step<A, J + 3, DUMP>(m1);
+    c[4] = mark_step<A, J + 4, DUMP>(m0); c[4] += mark_step<A, J + 4, DUMP>(m1);
+    c[5] = mark_step<A, J + 5, DUMP>(m0); c[5] += mark_step<A, J + 5, DUMP>(m1);
+    c[6] = mark_step<A, J + 6, DUMP>(m0); c[6] += mark_step<A, J + 6, DUMP>(m1);
+    c[7] = mark_step<A, J + 7, DUMP>(m0); c[7] += mark_step<A, J + 7, DUMP>(m1);
+    if (m0.U != U0) { m0.lb = J / 8 + 1; m0.lu = U0; }
+    if (m1.U != U1) { m1.lb = J / 8 + 1; m1.lu = U1; }
+    hist8(c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7], h + J, lane);
+}
+
+// phase 1: candidates [J, kP1) for two words per lane, no exit tests
+template <int A, int J, bool DUMP>
+__device__ __forceinline__ void phase1(Lane6 &m0, Lane6 &m1, uint32_t *h, int lane)
+{
+    if constexpr (J < kP1) {
+        block8x2<A, J, DUMP>(m0, m1, h, lane);
+        phase1<A, J + 8, DUMP>(m0, m1, h, lane);
+    }
+}
+
+// phase 2: candidates [J, kK) for one word per lane, warp exit test every 8
+template <int A, int J, bool DUMP>
+__device__ __forceinline__ void phase2(Lane6 &m, uint32_t *h, int lane)
+{
+    if constexpr (J < kK) {
+        if (!__any_sync(FULL, m.U != 0)) return;
+        block8<A, J, DUMP>(m, h, lane);
+        phase2<A, J + 8, DUMP>(m, h, lane);
+    }
+}
+
+// max p_min among the unrolled hits: replay the last block with a hit (from the U
+// saved at its start), only lanes holding the warp's latest block, and only when
+// that block can raise this warp's running maximum best_p
+template <int A>
+__device__ __forceinline__ void replay_key(const Lane6 &m, uint64_t u, const VerifyArgs &a,
+                                           uint32_t &best_p, Acc &acc)
+{
+    const uint32_t bstar = __reduce_max_sync(FULL, m.lb);
+    if (bstar == 0) return;
+    const ClassTable &T = c_tab[A / 2];
+    if (T.p[8 * bstar - 1] < best_p) return;
+    const uint32_t jr = (bstar - 1) * 8;
+    best_p = max(best_p, T.p[jr]);
+    if (m.lb != bstar) return;
+    uint32_t x = m.lu, lp = 0, lbits = 0;
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t p = T.p[jr + i];
+        const Trans t = trans(A, p);
+        const uint32_t *src = t.src ? m.wb : m.wa;
+        const int wa = (int)(t.shift >> 5);
+        const uint32_t S = __funnelshift_l(src[-wa - 1], src[-wa], t.shift & 31);
+        const uint32_t nw = x & S;
+        x ^= nw;
+        if (nw) { lp = p; lbits = nw; }
+    }
+    const uint64_t n = 6 * (u * 32 + (uint64_t)(__ffs(lbits) - 1)) + A;
+    const uint64_t key = make_key(lp, n, a.origin);
+    if (key > acc.key) acc.key = key;
+}
+
+// candidates past the unrolled tables (runtime loop over the resident list, class
+// filtered), then the exhaustive on-GPU fallback; folds the word into acc
+template <int A, bool DUMP>
+__device__ __forceinline__ void finish_word(uint32_t U, uint64_t word_sum, uint32_t j0, const uint32_t *wa,
+                                            const uint32_t *wb, uint64_t u, uint32_t *sh_hist,
+                                            const VerifyArgs &a, Acc &acc, int lane)
+{
+    uint32_t lastp = 0, lastb = 0;
+    for (uint32_t j = j0; j < a.n_cand; ++j) {
+        if (!__any_sync(FULL, U != 0)) break;
+        const uint32_t p = __ldg(a.sp.primes + j);
+        const Trans t = trans(A, p);
+        if (!t.ok) continue;
+        const uint32_t *src = t.src ? wb : wa;
+        const int wsh = (int)(t.shift >> 5);
+        const uint32_t S = __funnelshift_l(src[-wsh - 1], src[-wsh], t.shift & 31);
+        const uint32_t nw = U & S;
+        const uint32_t c = __popc(nw);
+        if (nw) {
+            U ^= nw;
+            word_sum += (uint64_t)c * p;
+            lastp = p; lastb = nw;
+            if (DUMP) {
+                uint32_t x = nw;
+                while (x) {
+                    const int b = __ffs(x) - 1;
+                    x &= x - 1;
+                    a.dump[(6 * (u * 32 + b) + A - a.lo_e) / 2] = p;
+                }
+            }
+        }
+        const uint32_t tot = __reduce_add_sync(FULL, c);
+        if (lane == 0 && tot) hist_add(sh_hist, a.result, j + 2, tot);
+    }
+    if (lastp) {
+        const uint64_t n = 6 * (u * 32 + (uint64_t)(__ffs(lastb) - 1)) + A;
+        const uint64_t key = make_key(lastp, n, a.origin);
+        if (key > acc.key) acc.key = key;
+    }
+    acc.fast_unres += __popc(U);
+    while (true) {
+        const uint32_t m = __ballot_sync(FULL, U != 0);
+        if (!m) break;
+        const int L = __ffs(m) - 1;
+        const uint32_t lw = __shfl_sync(FULL, U, L);
+        const uint64_t uL = __shfl_sync(FULL, u, L);
+        const int bit = __ffs(lw) - 1;
+        const uint64_t n = 6 * (uL * 32 + (uint64_t)bit) + A;
+        const uint64_t p = fallback_scan(n, a.p_fallback, a.cap, a.base_bits, a.R);
+        if (lane == L) {
+            U &= ~(1u << bit);
+            if (p) {
+                word_sum += p;
+                hist_add(sh_hist, a.result, bin_of_prime(p, a.sp.primes, a.n_base), 1);
+                const uint64_t key = make_key(p, n, a.origin);
+                if (key > acc.key) acc.key = key;
+            } else {
+                acc.unres += 1;
+                hist_add(sh_hist, a.result, 0, 1);
+                if (n < acc.first_unres) acc.first_unres = n;
+            }
+            if (DUMP) a.dump[(n - a.lo_e) / 2] = (uint32_t)p;
+        }
+    }
+    acc.sum += word_sum;
+    acc.chk += word_sum * u;                 // CHK weight floor(n / 192) = u for every bit
+}
+
+template <int A>
+__device__ __forceinline__ uint32_t valid_mask(uint64_t u, const VerifyArgs &a)
+{
+    const uint64_t mb = u * 32, lo = a.m_lo[A / 2], hi = a.m_hi[A / 2];
+    uint32_t U = FULL;
+    if (mb < lo) U = (lo - mb >= 32) ? 0u : (U << (lo - mb));
+    if (mb + 32 > hi) U &= (hi <= mb) ? 0u : (FULL >> (mb + 32 - hi));
+    return U;
+}
+
+// n = 4 (class 4, m = 0): p_min = 2, the only even p (reading R2); n = 6 (class 0,
+// m = 1): p_min = 3 with q = 3, the one partner the wheel windows do not hold
+template <int A, bool DUMP>
+__device__ __forceinline__ uint32_t take_special(uint32_t U, uint64_t u, uint32_t *sh_hist,
+                                                 const VerifyArgs &a, Acc &acc)
+{
+    if (u != 0) return U;
+    if (A == 4 && (U & 1u)) {
+        U &= ~1u;
+        acc.sum += 2;
+        atomicAdd(sh_hist + 1, 1u);
+        const uint64_t key = make_key(2, 4, a.origin);
+        if (key > acc.key) acc.key = key;
+        if (DUMP) a.dump[(4 - a.lo_e) / 2] = 2;
+    }
+    if (A == 0 && (U & 2u)) {
+        U &= ~2u;
+        acc.sum += 3;
+        atomicAdd(sh_hist + 2, 1u);
+        const uint64_t key = make_key(3, 6, a.origin);
+        if (key > acc.key) acc.key = key;
+        if (DUMP) a.dump[(6 - a.lo_e) / 2] = 3;
+    }
+    return U;
+}
+
+struct Shared6 {
+    uint32_t hist[kHistSmem];          // bins by prime index (runtime loop, fallback, specials)
+    uint32_t histc[3][kK];             // unrolled candidates, by class table index
+    uint32_t q_li[kThreads / 32][kQueue];
+    uint32_t q_U[kThreads / 32][kQueue];
+    uint32_t next_round;
+    uint32_t ns;
+};
+
+template <int A, bool DUMP, bool UNROLL>
+struct ClassWork {
+    // one phase-2 batch of `take` queued words of class A
+    static __device__ __forceinline__ void batch(Shared6 &sh, uint32_t &qn, uint32_t take, uint64_t u0,
+                                                 const uint32_t *wA, const uint32_t *wB, uint32_t halo,
+                                                 const VerifyArgs &a, Acc &acc, uint32_t &best_p, int lane,
+                                                 int warp)
+    {
+        const uint32_t e = qn - take;
+        uint32_t li = 0, U = 0;
+        if ((uint32_t)lane < take) { li = sh.q_li[warp][e + lane]; U = sh.q_U[warp][e + lane]; }
+        __syncwarp();
+        qn = e;
+        const uint64_t u = u0 + li;
+        Lane6 m;
+        m.wa = wA + halo + li;
+        m.wb = wB + halo + li;
+        m.U = U;
+        m.word_sum = 0;
+        m.lb = 0; m.lu = 0;
+        m.dump_w = DUMP ? a.dump + ((int64_t)(192 * u + A) - (int64_t)a.lo_e) / 2 : nullptr;
+        phase2<A, kP1, DUMP>(m, sh.histc[A / 2], lane);
+        replay_key<A>(m, u, a, best_p, acc);
+        constexpr uint32_t j_next = kTab[A / 2].bin[kK - 1] - 1;   // odd-list index after the table
+        finish_word<A, DUMP>(m.U, m.word_sum, j_next, m.wa, m.wb, u, sh.hist, a, acc, lane);
+    }
+
+    // one phase-1 round: words pair*64 + lane and pair*64 + 32 + lane of class A
+    static __device__ __forceinline__ void round(Shared6 &sh, uint32_t &qn, uint32_t pair, uint32_t tw,
+                                                 uint64_t u0, const uint32_t *wA, const uint32_t *wB,
+                                                 uint32_t halo, const VerifyArgs &a, Acc &acc,
+                                                 uint32_t &best_p, int lane, int warp)
+    {
+        const uint32_t li0 = pair * 64 + lane, li1 = li0 + 32;
+        const uint64_t ua = u0 + li0, ub = u0 + li1;
+        uint32_t Ua = li0 < tw ? valid_mask<A>(ua, a) : 0u;
+        uint32_t Ub = li1 < tw ? valid_mask<A>(ub, a) : 0u;
+        acc.evens += __popc(Ua) + __popc(Ub);
+        Ua = take_special<A, DUMP>(Ua, ua, sh.hist, a, acc);
+        const uint32_t c0 = li0 < tw ? li0 : tw - 1, c1 = li1 < tw ? li1 : tw - 1;
+        if constexpr (UNROLL) {
+            Lane6 m0, m1;
+            m0.wa = wA + halo + c0; m0.wb = wB + halo + c0;
+            m1.wa = wA + halo + c1; m1.wb = wB + halo + c1;
+            m0.U = Ua; m1.U = Ub;
+            m0.word_sum = m1.word_sum = 0;
+            m0.lb = m1.lb = 0; m0.lu = m1.lu = 0;
+            m0.dump_w = DUMP ? a.dump + ((int64_t)(192 * ua + A) - (int64_t)a.lo_e) / 2 : nullptr;
+            m1.dump_w = DUMP ? a.dump + ((int64_t)(192 * ub + A) - (int64_t)a.lo_e) / 2 : nullptr;
+            phase1<A, 0, DUMP>(m0, m1, sh.histc[A / 2], lane);
+            acc.sum += (uint64_t)m0.word_sum + m1.word_sum;
+            acc.chk += (uint64_t)m0.word_sum * ua + (uint64_t)m1.word_sum * ub;
+            replay_key<A>(m0, ua, a, best_p, acc);
+            replay_key<A>(m1, ub, a, best_p, acc);
+            uint32_t bal = __ballot_sync(FULL, m0.U != 0);
+            if (m0.U) {
+                const uint32_t pos = qn + __popc(bal & ((1u << lane) - 1));
+                sh.q_li[warp][pos] = li0;
+                sh.q_U[warp][pos] = m0.U;
+            }
+            qn += __popc(bal);
+            bal = __ballot_sync(FULL, m1.U != 0);
+            if (m1.U) {
+                const uint32_t pos = qn + __popc(bal & ((1u << lane) - 1));
+                sh.q_li[warp][pos] = li1;
+                sh.q_U[warp][pos] = m1.U;
+            }
+            qn += __popc(bal);
+            __syncwarp();
+            while (qn >= 32) batch(sh, qn, 32, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+        } else {
+            // p_max below the unrolled tables: runtime loop for every word (tests)
+            finish_word<A, DUMP>(Ua, 0, 0, wA + halo + c0, wB + halo + c0, ua, sh.hist, a, acc, lane);
+            finish_word<A, DUMP>(Ub, 0, 0, wA + halo + c1, wB + halo + c1, ub, sh.hist, a, acc, lane);
+        }
+    }
+};
+
+template <bool DUMP, bool UNROLL>
+__device__ __forceinline__ void flush_queue(int cls, Shared6 &sh, uint32_t &qn, uint64_t u0, const uint32_t *wA,
+                                            const uint32_t *wB, uint32_t halo, const VerifyArgs &a, Acc &acc,
+                                            uint32_t &best_p, int lane, int warp)
+{
+    if (!UNROLL || qn == 0) return;
+    if (cls == 0) ClassWork<0, DUMP, UNROLL>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+    else if (cls == 1) ClassWork<2, DUMP, UNROLL>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+    else ClassWork<4, DUMP, UNROLL>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+}
+
+// UNROLL: every unrolled candidate of the three class tables is <= p_max.
+template <bool DUMP, bool UNROLL>
+__global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
+{
+    extern __shared__ uint32_t win[];          // class A window | class B window
+    __shared__ Shared6 sh;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t halo = a.halo;
+    const uint32_t nw_max = halo + kTileWords;
+    uint32_t *wA = win, *wB = win + nw_max;
+    for (int i = tid; i < kHistSmem; i += kThreads) sh.hist[i] = 0;
+    for (int i = tid; i < 3 * kK; i += kThreads) (&sh.histc[0][0])[i] = 0;
+    Acc acc;
+    uint32_t best_p = 0;                       // per warp: replay only blocks that can raise the max
+    // contiguous run of tiles per CTA, so the sieve can carry its offsets
+    const uint64_t t_begin = (uint64_t)blockIdx.x * a.n_tiles / gridDim.x;
+    const uint64_t t_end = (uint64_t)(blockIdx.x + 1) * a.n_tiles / gridDim.x;
+    Carry6 cy;
+    cy.off = a.carry + (uint64_t)blockIdx.x * 2 * a.carry_stride;
+    cy.stride = a.carry_stride;
+    cy.n_carry = a.n_carry;
+    cy.have_prev = false;
+    cy.n_steady = 0;
+    uint32_t ns_run = 0;                       // thread 0: running steady count (monotone)
+
+    for (uint64_t tile = t_begin; tile < t_end; ++tile) {
+        const uint64_t u0 = a.u_first + tile * kTileWords;
+        const uint32_t tw = (uint32_t)min((uint64_t)kTileWords, a.u_end - u0);
+        const int64_t g0 = (int64_t)u0 - (int64_t)halo;
+        __syncthreads();                      // previous tile fully consumed
+        if (tid == 0) {
+            sh.next_round = 0;
+            // steady primes of this window: carried (previous tile done here) and
+            // p^2 <= 6 m_lo + 1, i.e. the progression started below the window
+            uint32_t ns = 0;
+            const int64_t m_lo = g0 * 32;
+            if (cy.have_prev && m_lo > 0) {
+                const uint64_t lim = 6 * (uint64_t)m_lo + 1;
+                const uint32_t top = min(cy.n_carry, a.sp.n_use);
+                ns = max(ns_run, a.sp.i_med);
+                if (ns == a.sp.i_med) {
+                    uint32_t lo = a.sp.i_med, hi = top;
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        const uint64_t pm = __ldg(a.sp.primes + mid);
+                        if (pm * pm <= lim) lo = mid + 1; else hi = mid;
+                    }
+                    ns = lo;
+                } else {
+                    while (ns < top) {
+                        const uint64_t pm = __ldg(a.sp.primes + ns);
+                        if (pm * pm > lim) break;
+                        ++ns;
+                    }
+                }
+                ns_run = ns;
+            }
+            sh.ns = ns;
+        }
+        __syncthreads();
+        cy.n_steady = sh.ns;
+        sieve6_window(wA, wB, g0, halo + tw, a.sp, &cy);
+        cy.have_prev = true;
+        __syncthreads();
+
+        // marking: rounds of 64 words of one class, handed out dynamically (class-major)
+        const uint32_t r1 = (tw + 63) >> 6;
+        uint32_t qn = 0;
+        int qcls = 0;
+        while (true) {
+            uint32_t r = 0;
+            if (lane == 0) r = atomicAdd(&sh.next_round, 1u);
+            r = __shfl_sync(FULL, r, 0);
+            if (r >= 3 * r1) break;
+            const int cls = (int)(r / r1);
+            const uint32_t pair = r - (uint32_t)cls * r1;
+            if (cls != qcls) {
+                flush_queue<DUMP, UNROLL>(qcls, sh, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+                qcls = cls;
+            }
+            if (cls == 0) ClassWork<0, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+            else if (cls == 1) ClassWork<2, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+            else ClassWork<4, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+        }
+        flush_queue<DUMP, UNROLL>(qcls, sh, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+
+        // per-tile flush of the shared histograms keeps their 32-bit bins exact
+        __syncthreads();
+        unsigned long long *R = (unsigned long long *)a.result;
+        for (int i = tid; i < kHistSmem; i += kThreads) {
+            const uint32_t v = sh.hist[i];
+            if (v) {
+                atomicAdd(R + GB_R_HIST + i, (unsigned long long)v);
+                sh.hist[i] = 0;
+            }
+        }
+        for (int i = tid; i < 3 * kK; i += kThreads) {
+            const uint32_t v = (&sh.histc[0][0])[i];
+            if (v) {
+                atomicAdd(R + GB_R_HIST + c_tab[i / kK].bin[i % kK], (unsigned long long)v);
+                (&sh.histc[0][0])[i] = 0;
+            }
+        }
+    }
+    acc.verified = acc.evens - acc.unres;
+
+    // flush: warp-reduce then one atomic per warp per field
+    auto wsum = [&](uint64_t v) {
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        return v;
+    };
+    auto wmax = [&](uint64_t v) {
+        for (int o = 16; o; o >>= 1) { uint64_t w = __shfl_xor_sync(FULL, v, o); v = w > v ? w : v; }
+        return v;
+    };
+    auto wmin = [&](uint64_t v) {
+        for (int o = 16; o; o >>= 1) { uint64_t w = __shfl_xor_sync(FULL, v, o); v = w < v ? w : v; }
+        return v;
+    };
+    const uint64_t ev = wsum(acc.evens), vf = wsum(acc.verified), fu = wsum(acc.fast_unres);
+    const uint64_t un = wsum(acc.unres), sm = wsum(acc.sum), ck = wsum(acc.chk);
+    const uint64_t ky = wmax(acc.key), fr = wmin(acc.first_unres);
+    unsigned long long *R = (unsigned long long *)a.result;
+    if (lane == 0) {
+        if (ev) atomicAdd(R + GB_R_EVENS, ev);
+        if (vf) atomicAdd(R + GB_R_VERIFIED, vf);
+        if (fu) atomicAdd(R + GB_R_FASTPATH_UNRESOLVED, fu);
+        if (un) atomicAdd(R + GB_R_UNRESOLVED, un);
+        if (sm) atomicAdd(R + GB_R_SUM_PMIN, sm);
+        if (ck) atomicAdd(R + GB_R_CHK_RAW, ck);
+        if (ky) atomicMax(R + GB_R_MAX_KEY, ky);
+        if (fr != UINT64_MAX) atomicMin(R + GB_R_FIRST_UNRESOLVED_N, fr);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+cudaError_t configure_verify(size_t smem_max)
+{
+    const int sm = (int)smem_max;
+    cudaError_t e = cudaFuncSetAttribute(verify_kernel<false, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(verify_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(verify_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(verify_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    return e;
+}
+
+int verify_blocks_per_sm(size_t smem)
+{
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, verify_kernel<false, true>, kThreads, smem) !=
+        cudaSuccess)
+        return 1;
+    return nb < 1 ? 1 : nb;
+}
+
+cudaError_t launch_verify(const VerifyArgs &a, int grid, size_t smem, cudaStream_t st)
+{
+    const bool unroll = a.p_fallback - 2 >= kUnrollPMax;   // p_fallback = largest candidate + 2
+    if (a.dump) {
+        if (unroll) verify_kernel<true, true><<<grid, kThreads, smem, st>>>(a);
+        else verify_kernel<true, false><<<grid, kThreads, smem, st>>>(a);
+    } else {
+        if (unroll) verify_kernel<false, true><<<grid, kThreads, smem, st>>>(a);
+        else verify_kernel<false, false><<<grid, kThreads, smem, st>>>(a);
+    }
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace gb

@@ -116,7 +116,7 @@ def test_brute_force_small():
     assert r["evens"] == len(want) and r["unresolved"] == 0
     assert r["sum_pmin"] == int(want.sum())
     ns = np.arange(4, hi, 2, dtype=np.uint64)
-    assert r["chk"] == int((want.astype(np.uint64) * ((ns - 4) // 64)).sum()) & U64
+    assert r["chk"] == int((want.astype(np.uint64) * (ns // 192)).sum()) & U64
     idx = prime_index_bins()
     h = np.zeros(oracle.NBINS, dtype=np.int64)
     for p in want:
