@@ -41,6 +41,16 @@ __host__ __device__ inline uint4 make_pk(uint32_t p)
     return make_uint4(p, kTileM % p, rA, rB);
 }
 
+// shared-memory window address (32-bit state-space address) and a no-return AND on it
+__device__ __forceinline__ uint32_t smem_addr(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void smem_and(uint32_t saddr, uint32_t mask)
+{
+    asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(saddr), "r"(mask) : "memory");
+}
+
 // ~(1 << (b % 32)) as one funnel-shift rotate
 __device__ __forceinline__ uint32_t clear_mask(uint32_t b)
 {
@@ -63,8 +73,9 @@ __device__ __forceinline__ bool is_prime_dev(uint64_t x, const uint64_t *bits, u
 
 // Minimal prime p in [p_start, min(n/2, cap)] (p_start odd) with n - p prime, or 0.
 // All 32 lanes call it with the same n; lane l tests p_start + 2l + 64i
-// ("tests all odd p ... with no upper bound on p").
-__device__ __forceinline__ uint64_t fallback_scan(uint64_t n, uint64_t p_start, uint64_t cap,
+// ("tests all odd p ... with no upper bound on p").  Cold path:
+// kept out of line so the hot loop stays small in the instruction cache.
+static __device__ __noinline__ uint64_t fallback_scan(uint64_t n, uint64_t p_start, uint64_t cap,
                                                   const uint64_t *bits, uint64_t R)
 {
     const int lane = threadIdx.x & 31;

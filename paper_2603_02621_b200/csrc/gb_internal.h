@@ -11,7 +11,10 @@
 namespace gb {
 
 // ---- tiling constants (tuned for sm_100a: 148 SMs, 228 KB smem / SM) ----
-constexpr int kThreads = 512;              // threads per CTA, every kernel
+#ifndef GB_THREADS
+#define GB_THREADS 1024
+#endif
+constexpr int kThreads = GB_THREADS;       // threads per CTA, every kernel
 constexpr int kTileWords = 8192;           // verify tile: 32-bit words per mod-6 class
 constexpr uint32_t kTileM = 32u * kTileWords;  // m-span of a tile (n = 6m + a): 786432 evens
 constexpr int kSieveTileWords = 16384;     // 32-bit words per gb_sieve_segment CTA

@@ -46,10 +46,10 @@ __host__ __device__ constexpr Trans trans(int a, uint32_t p)
 }
 
 #ifndef GB_K6
-#define GB_K6 96
+#define GB_K6 160
 #endif
 #ifndef GB_P1
-#define GB_P1 32
+#define GB_P1 48
 #endif
 constexpr int kK = GB_K6;        // unrolled candidates per class
 constexpr int kP1 = GB_P1;       // phase 1: candidates every word goes through
@@ -136,27 +136,35 @@ __device__ __forceinline__ uint32_t next_off6(uint32_t off, uint32_t p, uint32_t
     return om >= tm ? om - tm : om + p - tm;
 }
 
-__device__ __forceinline__ void mark_progression(uint32_t *w, uint32_t off, uint32_t p, uint32_t nbits,
-                                                 int lane)
+// clear bit b of the window at shared address w (word b / 32)
+__device__ __forceinline__ void clear_bit(uint32_t w, uint32_t b)
+{
+    smem_and(w + ((b >> 5) << 2), clear_mask(b));
+}
+
+__device__ __forceinline__ void mark_progression(uint32_t w, uint32_t off, uint32_t p, uint32_t nbits,
+                                                 uint32_t lane)
 {
     // one warp, one prime: lane l marks off + l p, off + (l + 32) p, ...
     const uint32_t stride = 32 * p;
     uint32_t b = off + lane * p;
     for (; b + 3 * stride < nbits; b += 4 * stride) {
         const uint32_t b1 = b + stride, b2 = b1 + stride, b3 = b2 + stride;
-        atomicAnd(w + (b >> 5), clear_mask(b));
-        atomicAnd(w + (b1 >> 5), clear_mask(b1));
-        atomicAnd(w + (b2 >> 5), clear_mask(b2));
-        atomicAnd(w + (b3 >> 5), clear_mask(b3));
+        clear_bit(w, b);
+        clear_bit(w, b1);
+        clear_bit(w, b2);
+        clear_bit(w, b3);
     }
-    for (; b < nbits; b += stride) atomicAnd(w + (b >> 5), clear_mask(b));
+    for (; b < nbits; b += stride) clear_bit(w, b);
 }
 
 __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
                               Carry6 *cy)
 {
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x;
+    const uint32_t lane = (uint32_t)tid & 31;
     constexpr int nt = kThreads;
+    const uint32_t sA = smem_addr(wA), sB = smem_addr(wB);
     // Phase T: primes 5..31 by shifted word patterns, per-thread incremental phases
     {
         int64_t g = g0 + tid;
@@ -253,8 +261,8 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
         if (pi >= m_end) break;
         const uint32_t p = __ldg(sp.primes + pi);
         const uint32_t oa = sh_mA[pi - sp.i_med], ob = sh_mB[pi - sp.i_med];
-        if (oa < nbits) mark_progression(wA, oa, p, nbits, lane);
-        if (ob < nbits) mark_progression(wB, ob, p, nbits, lane);
+        if (oa < nbits) mark_progression(sA, oa, p, nbits, lane);
+        if (ob < nbits) mark_progression(sB, ob, p, nbits, lane);
     }
     // large primes: one thread per prime.  Steady primes: kB in flight per thread.
     const uint32_t b_begin = sp.i_big > sp.i_med ? sp.i_big : sp.i_med;
@@ -280,8 +288,8 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
 #pragma unroll
         for (int k = 0; k < kB; ++k) {
             const uint32_t p = pt[k].x, tm = pt[k].y;
-            for (uint32_t b = oa[k]; b < nbits; b += p) atomicAnd(wA + (b >> 5), clear_mask(b));
-            for (uint32_t b = ob[k]; b < nbits; b += p) atomicAnd(wB + (b >> 5), clear_mask(b));
+            for (uint32_t b = oa[k]; b < nbits; b += p) clear_bit(sA, b);
+            for (uint32_t b = ob[k]; b < nbits; b += p) clear_bit(sB, b);
             const uint32_t pi = p0 + k * nt;
             if (pi < s_end) {
                 cy->off[pi] = oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm;
@@ -304,8 +312,8 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             oa = (uint32_t)first_hit6(k.x, k.z, mg, m_lo, m_hi);
             ob = (uint32_t)first_hit6(k.x, k.w, mg, m_lo, m_hi);
         }
-        for (uint32_t b = oa; b < nbits; b += k.x) atomicAnd(wA + (b >> 5), clear_mask(b));
-        for (uint32_t b = ob; b < nbits; b += k.x) atomicAnd(wB + (b >> 5), clear_mask(b));
+        for (uint32_t b = oa; b < nbits; b += k.x) clear_bit(sA, b);
+        for (uint32_t b = ob; b < nbits; b += k.x) clear_bit(sB, b);
         if (carried) {
             cy->off[pi] = next_off6(oa, k.x, k.y);
             cy->off[cy->stride + pi] = next_off6(ob, k.x, k.y);
@@ -563,8 +571,9 @@ struct Shared6 {
 
 template <int A, bool DUMP, bool UNROLL>
 struct ClassWork {
-    // one phase-2 batch of `take` queued words of class A
-    static __device__ __forceinline__ void batch(Shared6 &sh, uint32_t &qn, uint32_t take, uint64_t u0,
+    // one phase-2 batch of `take` queued words of class A (out of line: called from
+    // the round loop and the queue flushes; keeps the hot code small)
+    static __device__ __noinline__ void batch(Shared6 &sh, uint32_t &qn, uint32_t take, uint64_t u0,
                                                  const uint32_t *wA, const uint32_t *wB, uint32_t halo,
                                                  const VerifyArgs &a, Acc &acc, uint32_t &best_p, int lane,
                                                  int warp)
