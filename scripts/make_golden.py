@@ -86,6 +86,7 @@ def main():
         lo = hi
     total["hist"] = {str(k): v for k, v in sorted(total["hist"].items())}
     doc = {"lo": 4, "hi": N + 1, "p_fast": args.p_fast,
+           "chk_def": "sum p_min(n)*floor(n/192) mod 2^64 (DESIGN.md R6)",
            "source": "oracle/gb_oracle.c via scripts/make_golden.py (CPU oracle only)",
            "oracle_seconds": round(t_all, 1), "result": total}
     with open(outp, "w") as f:
