@@ -19,7 +19,10 @@ constexpr int kTileWords = 8192;           // verify tile: 32-bit words per mod-
 constexpr uint32_t kTileM = 32u * kTileWords;  // m-span of a tile (n = 6m + a): 786432 evens
 constexpr int kSieveTileWords = 16384;     // 32-bit words per gb_sieve_segment CTA
 constexpr int kHistSmem = 1024;            // histogram bins kept in shared memory
-constexpr uint32_t kWarpPrimeMax = 8192;   // primes <= this: one warp per prime
+#ifndef GB_WARP_PMAX
+#define GB_WARP_PMAX 8192
+#endif
+constexpr uint32_t kWarpPrimeMax = GB_WARP_PMAX;   // primes <= this: one warp per prime
 constexpr int kTinyPrimes = 10;            // 3..31 sieved by word patterns
 constexpr uint64_t kDumpScratch = 1ull << 24;  // u32 entries of host-API dump scratch
 constexpr int kScanBlockWords = 2048;      // u64 words per K-BASE compaction block

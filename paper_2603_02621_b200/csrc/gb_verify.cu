@@ -142,20 +142,24 @@ __device__ __forceinline__ void clear_bit(uint32_t w, uint32_t b)
     smem_and(w + ((b >> 5) << 2), clear_mask(b));
 }
 
-__device__ __forceinline__ void mark_progression(uint32_t w, uint32_t off, uint32_t p, uint32_t nbits,
+__device__ __forceinline__ void mark_progression(uint32_t w, uint32_t off, uint32_t p, uint32_t nw,
                                                  uint32_t lane)
 {
-    // one warp, one prime: lane l marks off + l p, off + (l + 32) p, ...
-    const uint32_t stride = 32 * p;
-    uint32_t b = off + lane * p;
-    for (; b + 3 * stride < nbits; b += 4 * stride) {
-        const uint32_t b1 = b + stride, b2 = b1 + stride, b3 = b2 + stride;
-        clear_bit(w, b);
-        clear_bit(w, b1);
-        clear_bit(w, b2);
-        clear_bit(w, b3);
+    // one warp, one prime: lane l marks bits off + l p + k 32p.  The stride is p
+    // whole words, so a lane's bit-in-word (hence its mask) never changes: only the
+    // word address moves, by 4p bytes per hit.
+    const uint32_t b0 = off + lane * p;
+    const uint32_t mask = clear_mask(b0);
+    const uint32_t step = 4 * p;
+    const uint32_t end = w + 4 * nw;
+    uint32_t ad = w + ((b0 >> 5) << 2);
+    for (; ad + 3 * step < end; ad += 4 * step) {
+        smem_and(ad, mask);
+        smem_and(ad + step, mask);
+        smem_and(ad + 2 * step, mask);
+        smem_and(ad + 3 * step, mask);
     }
-    for (; b < nbits; b += stride) clear_bit(w, b);
+    for (; ad < end; ad += step) smem_and(ad, mask);
 }
 
 __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
@@ -261,8 +265,8 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
         if (pi >= m_end) break;
         const uint32_t p = __ldg(sp.primes + pi);
         const uint32_t oa = sh_mA[pi - sp.i_med], ob = sh_mB[pi - sp.i_med];
-        if (oa < nbits) mark_progression(sA, oa, p, nbits, lane);
-        if (ob < nbits) mark_progression(sB, ob, p, nbits, lane);
+        if (oa < nbits) mark_progression(sA, oa, p, nw, lane);
+        if (ob < nbits) mark_progression(sB, ob, p, nw, lane);
     }
     // large primes: one thread per prime.  Steady primes: kB in flight per thread.
     const uint32_t b_begin = sp.i_big > sp.i_med ? sp.i_big : sp.i_med;
