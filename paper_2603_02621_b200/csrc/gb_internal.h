@@ -15,7 +15,10 @@ namespace gb {
 #define GB_THREADS 1024
 #endif
 constexpr int kThreads = GB_THREADS;       // threads per CTA, every kernel
-constexpr int kTileWords = 8192;           // verify tile: 32-bit words per mod-6 class
+#ifndef GB_TILE_WORDS
+#define GB_TILE_WORDS 20480
+#endif
+constexpr int kTileWords = GB_TILE_WORDS;  // verify tile: 32-bit words per mod-6 class
 constexpr uint32_t kTileM = 32u * kTileWords;  // m-span of a tile (n = 6m + a): 786432 evens
 constexpr int kSieveTileWords = 16384;     // 32-bit words per gb_sieve_segment CTA
 constexpr int kHistSmem = 1024;            // histogram bins kept in shared memory

@@ -27,6 +27,10 @@
 
 namespace gb {
 
+#ifdef GB_PROFILE_PHASES
+__device__ unsigned long long g_prof[5];
+#endif
+
 // ---------------------------------------------------------------------------
 // transitions and compile-time class tables
 // ---------------------------------------------------------------------------
@@ -53,7 +57,7 @@ __host__ __device__ constexpr Trans trans(int a, uint32_t p)
 #endif
 constexpr int kK = GB_K6;        // unrolled candidates per class
 constexpr int kP1 = GB_P1;       // phase 1: candidates every word goes through
-constexpr int kQueue = 128;      // per-warp survivor queue
+constexpr int kQueue = 96;       // per-warp survivor queue (<= 31 carried + 64 per round)
 static_assert(kK % 8 == 0 && kP1 % 8 == 0 && kP1 <= kK, "blocks of 8 candidates");
 
 struct ClassTable {
@@ -723,10 +727,19 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
             sh.ns = ns;
         }
         __syncthreads();
+#ifdef GB_PROFILE_PHASES
+        const long long t0 = clock64();
+#endif
         cy.n_steady = sh.ns;
         sieve6_window(wA, wB, g0, halo + tw, a.sp, &cy);
         cy.have_prev = true;
+#ifdef GB_PROFILE_PHASES
+        const long long t1 = clock64();
+#endif
         __syncthreads();
+#ifdef GB_PROFILE_PHASES
+        const long long t2 = clock64();
+#endif
 
         // marking: rounds of 64 words of one class, handed out dynamically (class-major)
         const uint32_t r1 = (tw + 63) >> 6;
@@ -748,9 +761,25 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
             else ClassWork<4, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, warp);
         }
         flush_queue<DUMP, UNROLL>(qcls, sh, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+#ifdef GB_PROFILE_PHASES
+        const long long t3 = clock64();
+#endif
 
         // per-tile flush of the shared histograms keeps their 32-bit bins exact
         __syncthreads();
+#ifdef GB_PROFILE_PHASES
+        const long long t4 = clock64();
+        if (lane == 0) {
+            atomicAdd(&g_prof[0], (unsigned long long)(t1 - t0));   // sieve (per warp)
+            atomicAdd(&g_prof[1], (unsigned long long)(t2 - t1));   // wait after sieve
+            atomicAdd(&g_prof[2], (unsigned long long)(t3 - t2));   // mark
+            atomicAdd(&g_prof[3], (unsigned long long)(t4 - t3));   // wait after mark
+            atomicAdd(&g_prof[4], 1ull);
+        }
+        if (blockIdx.x == 0 && tid == 0 && tile + 1 == t_end)
+            printf("GBPROF sieve=%llu sieve_wait=%llu mark=%llu mark_wait=%llu warp-tiles=%llu\n", g_prof[0],
+                   g_prof[1], g_prof[2], g_prof[3], g_prof[4]);
+#endif
         unsigned long long *R = (unsigned long long *)a.result;
         for (int i = tid; i < kHistSmem; i += kThreads) {
             const uint32_t v = sh.hist[i];
