@@ -6,6 +6,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <new>
 #include <vector>
 
@@ -31,8 +32,8 @@ constexpr uint64_t kMaxSms = 160;   // workspace sizing bound (B200: 148)
 
 struct Layout {
     uint64_t R, bits_words, list_cap, n_blk, carry_stride, carry_ctas;
-    uint64_t off_bits, off_primes, off_magic, off_tmod, off_carry, off_blk, off_counter, off_res,
-        off_dump, total;
+    uint64_t off_bits, off_primes, off_magic, off_tmod, off_carry, off_sched, off_blk, off_counter,
+        off_res, off_dump, total;
 };
 
 // pi(x) upper bound (Rosser-Schoenfeld: pi(x) < 1.25506 x / ln x for x > 1) + slack
@@ -64,6 +65,7 @@ bool plan(uint64_t hi_max, uint32_t p_max, Layout &L)
     L.off_magic = o;   o = align_up(o + 8 * L.list_cap, 256);
     L.off_tmod = o;    o = align_up(o + 16 * L.list_cap, 256);
     L.off_carry = o;   o = align_up(o + 8 * L.carry_stride * (uint64_t)kMaxBlocksPerSm * kMaxSms, 256);
+    L.off_sched = o;   o = align_up(o + 2 * 1024 + 4 * (kThreads / 32 + 1), 256);
     L.off_blk = o;     o = align_up(o + 8 * (L.n_blk + 1), 256);
     L.off_counter = o; o = align_up(o + 256, 256);
     L.off_res = o;     o = align_up(o + 8 * (uint64_t)GB_RESULT_WORDS, 256);
@@ -160,6 +162,8 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
     c->pk = (uint4 *)(ws + L.off_tmod);
     c->carry = (uint32_t *)(ws + L.off_carry);
     c->carry_stride = L.carry_stride;
+    c->med_idx = (uint16_t *)(ws + L.off_sched);
+    c->med_off = (uint32_t *)(ws + L.off_sched + 2 * 1024);
     c->blk = (uint64_t *)(ws + L.off_blk);
     c->counter = (uint32_t *)(ws + L.off_counter);
     c->res_scratch = (int64_t *)(ws + L.off_res);
@@ -212,6 +216,38 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
     if (cudaMemcpy(c->h_primes.data(), c->primes, 4ull * n_base, cudaMemcpyDeviceToHost) != cudaSuccess) {
         delete c;
         return GB_ECUDA;
+    }
+    // LPT schedule of the medium primes (31 < p <= kWarpPrimeMax) over the verify
+    // CTA's warps, by estimated marking work (hits per full window / 32 lanes + setup)
+    {
+        const uint32_t i_med = count_le(c->h_primes, 31), i_big = count_le(c->h_primes, kWarpPrimeMax);
+        const uint32_t nmed = i_big > i_med ? i_big - i_med : 0;
+        if (nmed > 1024) { delete c; return GB_EINTERNAL; }
+        const int nw = kThreads / 32;
+        const double nbits = 32.0 * (verify_halo(c->h_primes[count_le(c->h_primes, p_max) - 1]) + kTileWords);
+        std::vector<std::vector<uint16_t>> lists(nw);
+        std::vector<double> load(nw, 0.0);
+        for (uint32_t r = 0; r < nmed; ++r) {            // ascending p = descending work
+            const double p = c->h_primes[i_med + r];
+            const double cost = 2.0 * 3.0 * std::ceil(nbits / p / 32.0) + 30.0;
+            int best = 0;
+            for (int w = 1; w < nw; ++w)
+                if (load[w] < load[best]) best = w;
+            load[best] += cost;
+            lists[best].push_back((uint16_t)r);
+        }
+        std::vector<uint16_t> idx;
+        std::vector<uint32_t> off(1, 0);
+        for (int w = 0; w < nw; ++w) {
+            idx.insert(idx.end(), lists[w].begin(), lists[w].end());
+            off.push_back((uint32_t)idx.size());
+        }
+        if ((!idx.empty() && cudaMemcpy(c->med_idx, idx.data(), 2 * idx.size(), cudaMemcpyHostToDevice) !=
+                                 cudaSuccess) ||
+            cudaMemcpy(c->med_off, off.data(), 4 * off.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+            delete c;
+            return GB_ECUDA;
+        }
     }
     // verify kernel smem limit for the largest p_max this ctx accepts
     const uint32_t n_cand = count_le(c->h_primes, p_max);
@@ -325,6 +361,9 @@ gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_m
     a.carry_stride = ctx->carry_stride;
     a.n_carry = std::min<uint32_t>(a.sp.n_use, count_le(ctx->h_primes, kCarryPrimeMax));
     a.n_carry = (uint32_t)std::min<uint64_t>(a.n_carry, ctx->carry_stride);
+    a.med_idx = ctx->med_idx;
+    a.med_off = ctx->med_off;
+    a.i_b2 = count_le(ctx->h_primes, 16ull * (a.halo + kTileWords));   // 2p > 32 (halo + tile) bits
     return launch_verify(a, grid, smem, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
 }
 

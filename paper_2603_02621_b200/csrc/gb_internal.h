@@ -72,6 +72,9 @@ struct VerifyArgs {
     uint32_t *carry;          // per-CTA carried sieve offsets, 2 per prime (nullable)
     uint64_t carry_stride;    // u32 entries per class per CTA (row = 2 * carry_stride)
     uint32_t n_carry;         // primes [0, n_carry) carried
+    const uint16_t *med_idx;  // LPT schedule of the medium primes over the CTA's warps
+    const uint32_t *med_off;  // (kThreads/32 + 1 offsets)
+    uint32_t i_b2;            // first prime index with 2p > a full window (<= 2 hits per class)
 };
 
 // Launchers (gb_kernels.cu).  Each returns the cudaGetLastError() of its launch.
@@ -111,6 +114,8 @@ struct gb_ctx {
     uint32_t *carry;       // verify-kernel carried offsets: carry_ctas x carry_stride
     uint64_t carry_stride;
     uint32_t carry_ctas;
+    uint16_t *med_idx;     // LPT schedule of medium primes (host-computed, copied once)
+    uint32_t *med_off;
     uint64_t *blk;         // K-BASE scratch
     uint32_t *counter;     // K-BASE scratch
     int64_t *res_scratch;  // host API result

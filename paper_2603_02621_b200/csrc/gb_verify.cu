@@ -108,6 +108,11 @@ uint32_t unroll_p_max() { return kUnrollPMax; }
 // ---------------------------------------------------------------------------
 constexpr uint32_t kMedMax = 1024;
 
+struct MedSched {
+    const uint16_t *idx;     // medium prime (relative to i_med) per slot, grouped by warp
+    const uint32_t *off;     // warp w owns slots [off[w], off[w+1])
+};
+
 struct Carry6 {
     uint32_t *off;            // [0, stride): class A offsets, [stride, 2 stride): class B
     uint64_t stride;
@@ -156,18 +161,16 @@ __device__ __forceinline__ void mark_progression(uint32_t w, uint32_t off, uint3
     const uint32_t mask = clear_mask(b0);
     const uint32_t step = 4 * p;
     const uint32_t end = w + 4 * nw;
-    uint32_t ad = w + ((b0 >> 5) << 2);
-    for (; ad + 3 * step < end; ad += 4 * step) {
+    for (uint32_t ad = w + ((b0 >> 5) << 2); ad < end; ad += 4 * step) {   // 4 hits per trip, predicated
         smem_and(ad, mask);
-        smem_and(ad + step, mask);
-        smem_and(ad + 2 * step, mask);
-        smem_and(ad + 3 * step, mask);
+        if (ad + step < end) smem_and(ad + step, mask);
+        if (ad + 2 * step < end) smem_and(ad + 2 * step, mask);
+        if (ad + 3 * step < end) smem_and(ad + 3 * step, mask);
     }
-    for (; ad < end; ad += step) smem_and(ad, mask);
 }
 
 __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
-                              Carry6 *cy)
+                              Carry6 *cy, const MedSched &ms, uint32_t i_b2)
 {
     const int tid = threadIdx.x;
     const uint32_t lane = (uint32_t)tid & 31;
@@ -230,8 +233,6 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
     // handed out dynamically in ascending order (largest work first).
     const uint32_t m_end = sp.i_big < sp.n_use ? sp.i_big : sp.n_use;
     __shared__ uint32_t sh_mA[kMedMax], sh_mB[kMedMax];
-    __shared__ uint32_t sh_mnext;
-    if (tid == 0) sh_mnext = sp.i_med;
     for (uint32_t pi = sp.i_med + tid; pi < m_end; pi += nt) {
         const uint4 k = __ldg(sp.pk + pi);        // p, kTileM mod p, rA, rB
         uint32_t oa = 0xFFFFFFFFu, ob = 0xFFFFFFFFu;
@@ -262,28 +263,35 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
         sh_mB[pi - sp.i_med] = ob;
     }
     __syncthreads();
-    while (true) {
-        uint32_t pi = 0;
-        if (lane == 0) pi = atomicAdd(&sh_mnext, 1u);
-        pi = __shfl_sync(FULL, pi, 0);
-        if (pi >= m_end) break;
-        const uint32_t p = __ldg(sp.primes + pi);
-        const uint32_t oa = sh_mA[pi - sp.i_med], ob = sh_mB[pi - sp.i_med];
-        if (oa < nbits) mark_progression(sA, oa, p, nw, lane);
-        if (ob < nbits) mark_progression(sB, ob, p, nw, lane);
+    // one warp per medium prime: the host's LPT schedule (longest work first onto
+    // the least-loaded warp) gives every warp the same share, with no atomics
+    {
+        const uint32_t warp = (uint32_t)tid >> 5;
+        const uint32_t k0 = __ldg(ms.off + warp), k1 = __ldg(ms.off + warp + 1);
+        for (uint32_t k = k0; k < k1; ++k) {
+            const uint32_t rel = __ldg(ms.idx + k);
+            const uint32_t pi = sp.i_med + rel;
+            if (pi >= m_end) continue;
+            const uint32_t p = __ldg(sp.primes + pi);
+            const uint32_t oa = sh_mA[rel], ob = sh_mB[rel];
+            if (oa < nbits) mark_progression(sA, oa, p, nw, lane);
+            if (ob < nbits) mark_progression(sB, ob, p, nw, lane);
+        }
     }
     // large primes: one thread per prime.  Steady primes: kB in flight per thread.
     const uint32_t b_begin = sp.i_big > sp.i_med ? sp.i_big : sp.i_med;
     const uint32_t s_end = ns > b_begin ? (ns < sp.n_use ? ns : sp.n_use) : b_begin;
+    const uint32_t b2 = i_b2 < b_begin ? b_begin : (i_b2 < s_end ? i_b2 : s_end);
     constexpr int kB = 4;
-    for (uint32_t w0 = b_begin + (tid & ~31u); w0 < s_end; w0 += kB * nt) {   // warp-uniform trips
+    // steady primes with p <= full window / 2: hit loops (>= 2 hits per class)
+    for (uint32_t w0 = b_begin + (tid & ~31u); w0 < b2; w0 += kB * nt) {   // warp-uniform trips
         const uint32_t p0 = w0 + lane;
         uint2 pt[kB];
         uint32_t oa[kB], ob[kB];
 #pragma unroll
         for (int k = 0; k < kB; ++k) {
             const uint32_t pi = p0 + k * nt;
-            if (pi < s_end) {
+            if (pi < b2) {
                 const uint4 q = __ldg(sp.pk + pi);
                 pt[k] = make_uint2(q.x, q.y);
                 oa[k] = cy->off[pi];
@@ -299,12 +307,46 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             for (uint32_t b = oa[k]; b < nbits; b += p) clear_bit(sA, b);
             for (uint32_t b = ob[k]; b < nbits; b += p) clear_bit(sB, b);
             const uint32_t pi = p0 + k * nt;
-            if (pi < s_end) {
+            if (pi < b2) {
                 cy->off[pi] = oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm;
                 cy->off[cy->stride + pi] = ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm;
             }
         }
         __syncwarp();   // reconverge: the per-lane hit loops diverge
+    }
+    // steady primes with p > full window / 2: at most 2 hits per class, predicated,
+    // no loops and no divergence
+    constexpr int kB2 = 8;
+    for (uint32_t w0 = b2 + (tid & ~31u); w0 < s_end; w0 += kB2 * nt) {
+        const uint32_t p0 = w0 + lane;
+        uint2 pt[kB2];
+        uint32_t oa[kB2], ob[kB2];
+#pragma unroll
+        for (int k = 0; k < kB2; ++k) {
+            const uint32_t pi = p0 + k * nt;
+            if (pi < s_end) {
+                const uint4 q = __ldg(sp.pk + pi);
+                pt[k] = make_uint2(q.x, q.y);
+                oa[k] = cy->off[pi];
+                ob[k] = cy->off[cy->stride + pi];
+            } else {
+                pt[k] = make_uint2(nbits, 0);
+                oa[k] = ob[k] = nbits;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kB2; ++k) {
+            const uint32_t p = pt[k].x, tm = pt[k].y;
+            if (oa[k] < nbits) clear_bit(sA, oa[k]);
+            if (oa[k] + p < nbits) clear_bit(sA, oa[k] + p);
+            if (ob[k] < nbits) clear_bit(sB, ob[k]);
+            if (ob[k] + p < nbits) clear_bit(sB, ob[k] + p);
+            const uint32_t pi = p0 + k * nt;
+            if (pi < s_end) {
+                cy->off[pi] = oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm;
+                cy->off[cy->stride + pi] = ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm;
+            }
+        }
     }
     for (uint32_t pi = s_end + tid; pi < sp.n_use; pi += nt) {
         const uint4 k = __ldg(sp.pk + pi);
@@ -731,7 +773,7 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
         const long long t0 = clock64();
 #endif
         cy.n_steady = sh.ns;
-        sieve6_window(wA, wB, g0, halo + tw, a.sp, &cy);
+        sieve6_window(wA, wB, g0, halo + tw, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2);
         cy.have_prev = true;
 #ifdef GB_PROFILE_PHASES
         const long long t1 = clock64();
