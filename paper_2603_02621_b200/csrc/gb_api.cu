@@ -85,7 +85,15 @@ uint32_t count_le(const std::vector<uint32_t> &v, uint64_t x)
 
 // wheel halo: the largest shift of a candidate p is p/6 + 1 bits
 uint32_t verify_halo(uint32_t p_top) { return ((p_top / 6 + 1) >> 5) + 1; }
-size_t verify_smem(uint32_t halo) { return 2 * 4ull * (halo + kTileWords); }
+// the two class windows must fit next to the kernel's static shared memory
+constexpr uint32_t kVerifyDynSmemMax = 180 * 1024;
+uint32_t verify_tile_words(uint32_t halo)
+{
+    if (2 * 4ull * (halo + kTileWords) <= kVerifyDynSmemMax) return kTileWords;
+    const uint32_t tw = (kVerifyDynSmemMax / 8 - halo) & ~63u;     // multiple of 64 words
+    return tw;
+}
+size_t verify_smem(uint32_t halo) { return 2 * 4ull * (halo + verify_tile_words(halo)); }
 
 SievePrimes sieve_primes(const gb_ctx *c, uint64_t sqrt_bound)
 {
@@ -224,7 +232,8 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
         const uint32_t nmed = i_big > i_med ? i_big - i_med : 0;
         if (nmed > 1024) { delete c; return GB_EINTERNAL; }
         const int nw = kThreads / 32;
-        const double nbits = 32.0 * (verify_halo(c->h_primes[count_le(c->h_primes, p_max) - 1]) + kTileWords);
+        const uint32_t h0 = verify_halo(c->h_primes[count_le(c->h_primes, p_max) - 1]);
+        const double nbits = 32.0 * (h0 + verify_tile_words(h0));
         std::vector<std::vector<uint16_t>> lists(nw);
         std::vector<double> load(nw, 0.0);
         for (uint32_t r = 0; r < nmed; ++r) {            // ascending p = descending work
@@ -342,7 +351,8 @@ gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_m
     a.halo = verify_halo(p_top);
     a.u_first = mlo_min >> 5;
     a.u_end = ((mhi_max - 1) >> 5) + 1;
-    a.n_tiles = (a.u_end - a.u_first + kTileWords - 1) / kTileWords;
+    a.tile_words = verify_tile_words(a.halo);
+    a.n_tiles = (a.u_end - a.u_first + a.tile_words - 1) / a.tile_words;
     a.lo_e = lo_e;
     a.origin = ctx->origin;
     a.p_fallback = (uint64_t)p_top + 2;
@@ -363,7 +373,7 @@ gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_m
     a.n_carry = (uint32_t)std::min<uint64_t>(a.n_carry, ctx->carry_stride);
     a.med_idx = ctx->med_idx;
     a.med_off = ctx->med_off;
-    a.i_b2 = count_le(ctx->h_primes, 16ull * (a.halo + kTileWords));   // 2p > 32 (halo + tile) bits
+    a.i_b2 = count_le(ctx->h_primes, 16ull * (a.halo + a.tile_words));   // 2p > 32 (halo + tile) bits
     return launch_verify(a, grid, smem, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
 }
 

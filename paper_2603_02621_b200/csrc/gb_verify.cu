@@ -118,8 +118,17 @@ struct Carry6 {
     uint64_t stride;
     uint32_t n_carry;
     uint32_t n_steady;        // primes [i_med, n_steady): carried, p^2 <= 6 m_lo + 1
+    uint32_t tile_m;          // m-span of a tile (window step); kTileM unless p_max forces a smaller tile
     bool have_prev;
 };
+
+// (tile_m mod p): precomputed in pk.y for the default tile, else computed
+template <bool DEF_TILE>
+__device__ __forceinline__ uint32_t tile_mod(const Carry6 *cy, uint4 k)
+{
+    if constexpr (DEF_TILE) return k.y;
+    else return cy->tile_m % k.x;
+}
 
 __host__ __device__ constexpr uint32_t inv6(uint32_t p) { return p % 6 == 1 ? (5 * p + 1) / 6 : (p + 1) / 6; }
 __host__ __device__ constexpr uint32_t rA_of(uint32_t p) { return p - inv6(p); }
@@ -137,10 +146,10 @@ __device__ __forceinline__ uint64_t first_hit6(uint32_t p, uint32_t r, uint64_t 
     return ms + delta - (uint64_t)m_lo;
 }
 
-// next tile's first hit (the window moves up by kTileM)
-__device__ __forceinline__ uint32_t next_off6(uint32_t off, uint32_t p, uint32_t tm)
+// next tile's first hit (the window moves up by tile_m)
+__device__ __forceinline__ uint32_t next_off6(uint32_t off, uint32_t p, uint32_t tm, uint32_t tile_m)
 {
-    if (off >= kTileM) return off - kTileM;
+    if (off >= tile_m) return off - tile_m;
     const uint32_t om = off < p ? off : off % p;   // off >= p only when p^2 fell in this window
     return om >= tm ? om - tm : om + p - tm;
 }
@@ -169,6 +178,7 @@ __device__ __forceinline__ void mark_progression(uint32_t w, uint32_t off, uint3
     }
 }
 
+template <bool DEF_TILE>
 __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
                               Carry6 *cy, const MedSched &ms, uint32_t i_b2)
 {
@@ -240,12 +250,13 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
         if (pi < ns) {
             oa = cy->off[pi];
             ob = cy->off[cy->stride + pi];
-            cy->off[pi] = oa >= k.y ? oa - k.y : oa + k.x - k.y;
-            cy->off[cy->stride + pi] = ob >= k.y ? ob - k.y : ob + k.x - k.y;
+            const uint32_t tm = tile_mod<DEF_TILE>(cy, k);
+            cy->off[pi] = oa >= tm ? oa - tm : oa + k.x - tm;
+            cy->off[cy->stride + pi] = ob >= tm ? ob - tm : ob + k.x - tm;
         } else {
             const int64_t mmin = (int64_t)(((uint64_t)k.x * k.x - 1) / 6);
             if (mmin < m_hi) {
-                if (carried && cy->have_prev && mmin < m_hi - (int64_t)kTileM) {
+                if (carried && cy->have_prev && mmin < m_hi - (int64_t)cy->tile_m) {
                     oa = cy->off[pi];
                     ob = cy->off[cy->stride + pi];
                 } else {
@@ -254,8 +265,9 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
                     ob = (uint32_t)first_hit6(k.x, k.w, mg, m_lo, m_hi);
                 }
                 if (carried) {
-                    cy->off[pi] = next_off6(oa, k.x, k.y);
-                    cy->off[cy->stride + pi] = next_off6(ob, k.x, k.y);
+                    const uint32_t tm = tile_mod<DEF_TILE>(cy, k);
+                    cy->off[pi] = next_off6(oa, k.x, tm, cy->tile_m);
+                    cy->off[cy->stride + pi] = next_off6(ob, k.x, tm, cy->tile_m);
                 }
             }
         }
@@ -293,7 +305,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             const uint32_t pi = p0 + k * nt;
             if (pi < b2) {
                 const uint4 q = __ldg(sp.pk + pi);
-                pt[k] = make_uint2(q.x, q.y);
+                pt[k] = make_uint2(q.x, tile_mod<DEF_TILE>(cy, q));
                 oa[k] = cy->off[pi];
                 ob[k] = cy->off[cy->stride + pi];
             } else {
@@ -326,7 +338,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             const uint32_t pi = p0 + k * nt;
             if (pi < s_end) {
                 const uint4 q = __ldg(sp.pk + pi);
-                pt[k] = make_uint2(q.x, q.y);
+                pt[k] = make_uint2(q.x, tile_mod<DEF_TILE>(cy, q));
                 oa[k] = cy->off[pi];
                 ob[k] = cy->off[cy->stride + pi];
             } else {
@@ -354,7 +366,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
         if (mmin >= m_hi) break;
         const bool carried = pi < cy->n_carry;
         uint32_t oa, ob;
-        if (carried && cy->have_prev && mmin < m_hi - (int64_t)kTileM) {
+        if (carried && cy->have_prev && mmin < m_hi - (int64_t)cy->tile_m) {
             oa = cy->off[pi];
             ob = cy->off[cy->stride + pi];
         } else {
@@ -365,8 +377,9 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
         for (uint32_t b = oa; b < nbits; b += k.x) clear_bit(sA, b);
         for (uint32_t b = ob; b < nbits; b += k.x) clear_bit(sB, b);
         if (carried) {
-            cy->off[pi] = next_off6(oa, k.x, k.y);
-            cy->off[cy->stride + pi] = next_off6(ob, k.x, k.y);
+            const uint32_t tm = tile_mod<DEF_TILE>(cy, k);
+            cy->off[pi] = next_off6(oa, k.x, tm, cy->tile_m);
+            cy->off[cy->stride + pi] = next_off6(ob, k.x, tm, cy->tile_m);
         }
     }
 }
@@ -717,7 +730,7 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
     __shared__ Shared6 sh;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t halo = a.halo;
-    const uint32_t nw_max = halo + kTileWords;
+    const uint32_t nw_max = halo + a.tile_words;
     uint32_t *wA = win, *wB = win + nw_max;
     for (int i = tid; i < kHistSmem; i += kThreads) sh.hist[i] = 0;
     for (int i = tid; i < 3 * kK; i += kThreads) (&sh.histc[0][0])[i] = 0;
@@ -732,11 +745,12 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
     cy.n_carry = a.n_carry;
     cy.have_prev = false;
     cy.n_steady = 0;
+    cy.tile_m = 32 * a.tile_words;
     uint32_t ns_run = 0;                       // thread 0: running steady count (monotone)
 
     for (uint64_t tile = t_begin; tile < t_end; ++tile) {
-        const uint64_t u0 = a.u_first + tile * kTileWords;
-        const uint32_t tw = (uint32_t)min((uint64_t)kTileWords, a.u_end - u0);
+        const uint64_t u0 = a.u_first + tile * a.tile_words;
+        const uint32_t tw = (uint32_t)min((uint64_t)a.tile_words, a.u_end - u0);
         const int64_t g0 = (int64_t)u0 - (int64_t)halo;
         __syncthreads();                      // previous tile fully consumed
         if (tid == 0) {
@@ -773,7 +787,10 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
         const long long t0 = clock64();
 #endif
         cy.n_steady = sh.ns;
-        sieve6_window(wA, wB, g0, halo + tw, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2);
+        if (cy.tile_m == kTileM)
+            sieve6_window<true>(wA, wB, g0, halo + tw, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2);
+        else
+            sieve6_window<false>(wA, wB, g0, halo + tw, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2);
         cy.have_prev = true;
 #ifdef GB_PROFILE_PHASES
         const long long t1 = clock64();
