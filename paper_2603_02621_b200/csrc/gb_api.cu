@@ -86,14 +86,19 @@ uint32_t count_le(const std::vector<uint32_t> &v, uint64_t x)
 // wheel halo: the largest shift of a candidate p is p/6 + 1 bits
 uint32_t verify_halo(uint32_t p_top) { return ((p_top / 6 + 1) >> 5) + 1; }
 // the two class windows must fit next to the kernel's static shared memory
-constexpr uint32_t kVerifyDynSmemMax = 180 * 1024;
+constexpr uint32_t kVerifyDynSmemMax = 168 * 1024;   // the two windows; + queues + static <= 227 KB
+constexpr uint32_t kWinSlackWords = 128;   // = kWinSlack in gb_verify.cu
 uint32_t verify_tile_words(uint32_t halo)
 {
-    if (2 * 4ull * (halo + kTileWords) <= kVerifyDynSmemMax) return kTileWords;
-    const uint32_t tw = (kVerifyDynSmemMax / 8 - halo) & ~63u;     // multiple of 64 words
+    if (2 * 4ull * (halo + kTileWords + kWinSlackWords) <= kVerifyDynSmemMax) return kTileWords;
+    const uint32_t tw = (kVerifyDynSmemMax / 8 - halo - kWinSlackWords) & ~127u;   // multiple of 128 words
     return tw;
 }
-size_t verify_smem(uint32_t halo) { return 2 * 4ull * (halo + verify_tile_words(halo)); }
+constexpr size_t kQueueBytes = (kThreads / 32) * 160 * 6;   // per-warp survivor queues (u32 U + u16 index)
+size_t verify_smem(uint32_t halo)
+{
+    return 2 * 4ull * (halo + verify_tile_words(halo) + kWinSlackWords) + kQueueBytes;
+}
 
 SievePrimes sieve_primes(const gb_ctx *c, uint64_t sqrt_bound)
 {

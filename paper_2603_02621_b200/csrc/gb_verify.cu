@@ -57,8 +57,10 @@ __host__ __device__ constexpr Trans trans(int a, uint32_t p)
 #endif
 constexpr int kK = GB_K6;        // unrolled candidates per class
 constexpr int kP1 = GB_P1;       // phase 1: candidates every word goes through
-constexpr int kQueue = 96;       // per-warp survivor queue (<= 31 carried + 64 per round)
+constexpr uint32_t kWinSlack = 128;   // words past a window that phase-1 lanes may read (U = 0)
+constexpr int kQueue = 160;      // per-warp survivor queue (<= 31 carried + 32 kW per round)
 static_assert(kK % 8 == 0 && kP1 % 8 == 0 && kP1 <= kK, "blocks of 8 candidates");
+
 
 struct ClassTable {
     uint32_t p[kK];
@@ -478,6 +480,87 @@ __device__ __forceinline__ void phase1(Lane6 &m0, Lane6 &m1, uint32_t *h, int la
     }
 }
 
+// ---- phase 1 with kW words per lane (words li, li + 32, ..., li + 32(kW-1)) ----
+#ifndef GB_W1
+#define GB_W1 4
+#endif
+constexpr int kW = GB_W1;
+static_assert(kW * 32 * 32 < 65536, "16-bit packed per-warp counts");
+
+struct LaneQ {
+    const uint32_t *wa, *wb;   // class A / B window words aligned with word 0 (word k at +32k)
+    uint32_t U[kW];
+    uint32_t ws[kW];           // sum of p_min of resolved bits, per word
+    uint32_t lb[kW], lu[kW];   // TRACK: last block with a hit and U at its start
+    uint32_t *dump0;           // DUMP: dump entry of bit 0 of word 0 (word k at +3072k, bit b at +3b)
+};
+
+template <int A, int J, bool DUMP>
+__device__ __forceinline__ uint32_t qstep(LaneQ &m, int k)
+{
+    constexpr uint32_t P = kTab[A / 2].p[J];
+    constexpr Trans T = trans(A, P);
+    constexpr int WA = (int)(T.shift >> 5);
+    constexpr uint32_t WB = T.shift & 31;
+    const uint32_t *src = (T.src ? m.wb : m.wa) + 32 * k;
+    const uint32_t S = __funnelshift_l(src[-(WA + 1)], src[-WA], WB);
+    const uint32_t nw = m.U[k] & S;
+    m.U[k] ^= nw;
+    const uint32_t c = __popc(nw);
+    m.ws[k] += c * P;
+    if constexpr (DUMP) {
+        uint32_t x = nw;
+        while (x) {
+            const int b = __ffs(x) - 1;
+            x &= x - 1;
+            m.dump0[3072 * k + 3 * b] = P;
+        }
+    }
+    return c;
+}
+
+template <int A, int J, bool DUMP>
+__device__ __forceinline__ uint32_t qprime(LaneQ &m)
+{
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < kW; ++k) c += qstep<A, J, DUMP>(m, k);
+    return c;
+}
+
+template <int A, int J, bool DUMP, bool TRACK>
+__device__ __forceinline__ void block8q(LaneQ &m, uint32_t *h, int lane)
+{
+    uint32_t Ub[kW];
+    if constexpr (TRACK) {
+#pragma unroll
+        for (int k = 0; k < kW; ++k) Ub[k] = m.U[k];
+    }
+    const uint32_t c0 = qprime<A, J + 0, DUMP>(m);
+    const uint32_t c1 = qprime<A, J + 1, DUMP>(m);
+    const uint32_t c2 = qprime<A, J + 2, DUMP>(m);
+    const uint32_t c3 = qprime<A, J + 3, DUMP>(m);
+    const uint32_t c4 = qprime<A, J + 4, DUMP>(m);
+    const uint32_t c5 = qprime<A, J + 5, DUMP>(m);
+    const uint32_t c6 = qprime<A, J + 6, DUMP>(m);
+    const uint32_t c7 = qprime<A, J + 7, DUMP>(m);
+    if constexpr (TRACK) {
+#pragma unroll
+        for (int k = 0; k < kW; ++k)
+            if (m.U[k] != Ub[k]) { m.lb[k] = J / 8 + 1; m.lu[k] = Ub[k]; }
+    }
+    hist8(c0, c1, c2, c3, c4, c5, c6, c7, h + J, lane);   // per warp and prime <= 32 kW 32 hits
+}
+
+template <int A, int J, bool DUMP, bool TRACK>
+__device__ __forceinline__ void phase1q(LaneQ &m, uint32_t *h, int lane)
+{
+    if constexpr (J < kP1) {
+        block8q<A, J, DUMP, TRACK>(m, h, lane);
+        phase1q<A, J + 8, DUMP, TRACK>(m, h, lane);
+    }
+}
+
 // phase 2: candidates [J, kK) for one word per lane, warp exit test every 8
 template <int A, int J, bool DUMP>
 __device__ __forceinline__ void phase2(Lane6 &m, uint32_t *h, int lane)
@@ -517,6 +600,39 @@ __device__ __forceinline__ void replay_key(const Lane6 &m, uint64_t u, const Ver
     const uint64_t n = 6 * (u * 32 + (uint64_t)(__ffs(lbits) - 1)) + A;
     const uint64_t key = make_key(lp, n, a.origin);
     if (key > acc.key) acc.key = key;
+}
+
+template <int A>
+__device__ __forceinline__ void replay_key_q(const LaneQ &m, uint64_t u0w, const VerifyArgs &a, uint32_t &best_p,
+                                             Acc &acc)
+{
+    uint32_t mx = 0;
+#pragma unroll
+    for (int k = 0; k < kW; ++k) mx = max(mx, m.lb[k]);
+    const uint32_t bstar = __reduce_max_sync(FULL, mx);
+    if (bstar == 0) return;
+    const ClassTable &T = c_tab[A / 2];
+    if (T.p[8 * bstar - 1] < best_p) return;
+    const uint32_t jr = (bstar - 1) * 8;
+    best_p = max(best_p, T.p[jr]);
+#pragma unroll
+    for (int k = 0; k < kW; ++k) {
+        if (m.lb[k] != bstar) continue;
+        uint32_t x = m.lu[k], lp = 0, lbits = 0;
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t p = T.p[jr + i];
+            const Trans t = trans(A, p);
+            const uint32_t *src = (t.src ? m.wb : m.wa) + 32 * k;
+            const int wa = (int)(t.shift >> 5);
+            const uint32_t S = __funnelshift_l(src[-wa - 1], src[-wa], t.shift & 31);
+            const uint32_t nw = x & S;
+            x ^= nw;
+            if (nw) { lp = p; lbits = nw; }
+        }
+        const uint64_t n = 6 * ((u0w + 32 * k) * 32 + (uint64_t)(__ffs(lbits) - 1)) + A;
+        const uint64_t key = make_key(lp, n, a.origin);
+        if (key > acc.key) acc.key = key;
+    }
 }
 
 // candidates past the unrolled tables (runtime loop over the resident list, class
@@ -623,14 +739,25 @@ __device__ __forceinline__ uint32_t take_special(uint32_t U, uint64_t u, uint32_
     return U;
 }
 
+// dynamic shared memory: class A window | class B window | per-warp survivor queues
+extern __shared__ uint32_t g_win[];
+
 struct Shared6 {
     uint32_t hist[kHistSmem];          // bins by prime index (runtime loop, fallback, specials)
     uint32_t histc[3][kK];             // unrolled candidates, by class table index
-    uint32_t q_li[kThreads / 32][kQueue];
-    uint32_t q_U[kThreads / 32][kQueue];
     uint32_t next_round;
     uint32_t ns;
+    uint32_t q_base;      // word offset of the queues in dynamic shared memory
 };
+
+__device__ __forceinline__ uint32_t *sh_qU(const Shared6 &sh, int warp)
+{
+    return g_win + sh.q_base + (uint32_t)warp * kQueue;
+}
+__device__ __forceinline__ uint16_t *sh_qli(const Shared6 &sh, int warp)
+{
+    return (uint16_t *)(g_win + sh.q_base + (kThreads / 32) * kQueue) + (uint32_t)warp * kQueue;
+}
 
 template <int A, bool DUMP, bool UNROLL>
 struct ClassWork {
@@ -643,7 +770,7 @@ struct ClassWork {
     {
         const uint32_t e = qn - take;
         uint32_t li = 0, U = 0;
-        if ((uint32_t)lane < take) { li = sh.q_li[warp][e + lane]; U = sh.q_U[warp][e + lane]; }
+        if ((uint32_t)lane < take) { li = sh_qli(sh, warp)[e + lane]; U = sh_qU(sh, warp)[e + lane]; }
         __syncwarp();
         qn = e;
         const uint64_t u = u0 + li;
@@ -660,53 +787,73 @@ struct ClassWork {
         finish_word<A, DUMP>(m.U, m.word_sum, j_next, m.wa, m.wb, u, sh.hist, a, acc, lane);
     }
 
-    // one phase-1 round: words pair*64 + lane and pair*64 + 32 + lane of class A
+    // one phase-1 round: words pair*32kW + 32k + lane (k < kW) of class A
+    template <bool TRACK>
+    static __device__ __forceinline__ void round_q(Shared6 &sh, uint32_t &qn, uint32_t pair, uint32_t tw,
+                                                   uint64_t u0, const uint32_t *wA, const uint32_t *wB,
+                                                   uint32_t halo, const VerifyArgs &a, Acc &acc,
+                                                   uint32_t &best_p, int lane, int warp)
+    {
+        const uint32_t li0 = pair * 32 * kW + lane;
+        LaneQ m;
+        m.wa = wA + halo + li0;           // words past tw read window slack; their U is 0
+        m.wb = wB + halo + li0;
+        m.dump0 = DUMP ? a.dump + ((int64_t)(192 * (u0 + li0) + A) - (int64_t)a.lo_e) / 2 : nullptr;
+#pragma unroll
+        for (int k = 0; k < kW; ++k) {
+            const uint32_t li = li0 + 32 * k;
+            uint32_t U = li < tw ? valid_mask<A>(u0 + li, a) : 0u;
+            acc.evens += __popc(U);
+            if (k == 0) U = take_special<A, DUMP>(U, u0 + li, sh.hist, a, acc);
+            m.U[k] = U;
+            m.ws[k] = 0;
+            if (TRACK) { m.lb[k] = 0; m.lu[k] = 0; }
+        }
+        phase1q<A, 0, DUMP, TRACK>(m, sh.histc[A / 2], lane);
+#pragma unroll
+        for (int k = 0; k < kW; ++k) {
+            acc.sum += m.ws[k];
+            acc.chk += (uint64_t)m.ws[k] * (u0 + li0 + 32 * k);
+        }
+        if (TRACK) replay_key_q<A>(m, u0 + li0, a, best_p, acc);
+        // enqueue survivors
+#pragma unroll
+        for (int k = 0; k < kW; ++k) {
+            const uint32_t bal = __ballot_sync(FULL, m.U[k] != 0);
+            if (m.U[k]) {
+                const uint32_t pos = qn + __popc(bal & ((1u << lane) - 1));
+                sh_qli(sh, warp)[pos] = (uint16_t)(li0 + 32 * k);
+                sh_qU(sh, warp)[pos] = m.U[k];
+            }
+            qn += __popc(bal);
+        }
+        __syncwarp();
+        while (qn >= 32) batch(sh, qn, 32, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+    }
+
     static __device__ __forceinline__ void round(Shared6 &sh, uint32_t &qn, uint32_t pair, uint32_t tw,
                                                  uint64_t u0, const uint32_t *wA, const uint32_t *wB,
                                                  uint32_t halo, const VerifyArgs &a, Acc &acc,
                                                  uint32_t &best_p, int lane, int warp)
     {
-        const uint32_t li0 = pair * 64 + lane, li1 = li0 + 32;
-        const uint64_t ua = u0 + li0, ub = u0 + li1;
-        uint32_t Ua = li0 < tw ? valid_mask<A>(ua, a) : 0u;
-        uint32_t Ub = li1 < tw ? valid_mask<A>(ub, a) : 0u;
-        acc.evens += __popc(Ua) + __popc(Ub);
-        Ua = take_special<A, DUMP>(Ua, ua, sh.hist, a, acc);
-        const uint32_t c0 = li0 < tw ? li0 : tw - 1, c1 = li1 < tw ? li1 : tw - 1;
         if constexpr (UNROLL) {
-            Lane6 m0, m1;
-            m0.wa = wA + halo + c0; m0.wb = wB + halo + c0;
-            m1.wa = wA + halo + c1; m1.wb = wB + halo + c1;
-            m0.U = Ua; m1.U = Ub;
-            m0.word_sum = m1.word_sum = 0;
-            m0.lb = m1.lb = 0; m0.lu = m1.lu = 0;
-            m0.dump_w = DUMP ? a.dump + ((int64_t)(192 * ua + A) - (int64_t)a.lo_e) / 2 : nullptr;
-            m1.dump_w = DUMP ? a.dump + ((int64_t)(192 * ub + A) - (int64_t)a.lo_e) / 2 : nullptr;
-            phase1<A, 0, DUMP>(m0, m1, sh.histc[A / 2], lane);
-            acc.sum += (uint64_t)m0.word_sum + m1.word_sum;
-            acc.chk += (uint64_t)m0.word_sum * ua + (uint64_t)m1.word_sum * ub;
-            replay_key<A>(m0, ua, a, best_p, acc);
-            replay_key<A>(m1, ub, a, best_p, acc);
-            uint32_t bal = __ballot_sync(FULL, m0.U != 0);
-            if (m0.U) {
-                const uint32_t pos = qn + __popc(bal & ((1u << lane) - 1));
-                sh.q_li[warp][pos] = li0;
-                sh.q_U[warp][pos] = m0.U;
-            }
-            qn += __popc(bal);
-            bal = __ballot_sync(FULL, m1.U != 0);
-            if (m1.U) {
-                const uint32_t pos = qn + __popc(bal & ((1u << lane) - 1));
-                sh.q_li[warp][pos] = li1;
-                sh.q_U[warp][pos] = m1.U;
-            }
-            qn += __popc(bal);
-            __syncwarp();
-            while (qn >= 32) batch(sh, qn, 32, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+            // max-key tracking only while phase-1 primes can still raise this warp's max
+            constexpr uint32_t kP1Max = kTab[A / 2].p[kP1 - 1];
+            if (best_p > kP1Max)
+                round_q<false>(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+            else
+                round_q<true>(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, warp);
         } else {
             // p_max below the unrolled tables: runtime loop for every word (tests)
-            finish_word<A, DUMP>(Ua, 0, 0, wA + halo + c0, wB + halo + c0, ua, sh.hist, a, acc, lane);
-            finish_word<A, DUMP>(Ub, 0, 0, wA + halo + c1, wB + halo + c1, ub, sh.hist, a, acc, lane);
+            const uint32_t li0 = pair * 32 * kW + lane;
+            for (int k = 0; k < kW; ++k) {
+                const uint32_t li = li0 + 32 * k;
+                const uint64_t u = u0 + li;
+                uint32_t U = li < tw ? valid_mask<A>(u, a) : 0u;
+                acc.evens += __popc(U);
+                if (k == 0) U = take_special<A, DUMP>(U, u, sh.hist, a, acc);
+                finish_word<A, DUMP>(U, 0, 0, wA + halo + li, wB + halo + li, u, sh.hist, a, acc, lane);
+            }
         }
     }
 };
@@ -726,12 +873,13 @@ __device__ __forceinline__ void flush_queue(int cls, Shared6 &sh, uint32_t &qn, 
 template <bool DUMP, bool UNROLL>
 __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
 {
-    extern __shared__ uint32_t win[];          // class A window | class B window
+    uint32_t *win = g_win;                     // class A window | class B window | queues
     __shared__ Shared6 sh;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t halo = a.halo;
-    const uint32_t nw_max = halo + a.tile_words;
+    const uint32_t nw_max = halo + a.tile_words + kWinSlack;
     uint32_t *wA = win, *wB = win + nw_max;
+    if (tid == 0) sh.q_base = 2 * nw_max;
     for (int i = tid; i < kHistSmem; i += kThreads) sh.hist[i] = 0;
     for (int i = tid; i < 3 * kK; i += kThreads) (&sh.histc[0][0])[i] = 0;
     Acc acc;
@@ -801,7 +949,7 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
 #endif
 
         // marking: rounds of 64 words of one class, handed out dynamically (class-major)
-        const uint32_t r1 = (tw + 63) >> 6;
+        const uint32_t r1 = (tw + 32 * kW - 1) / (32 * kW);
         uint32_t qn = 0;
         int qcls = 0;
         while (true) {
