@@ -53,7 +53,7 @@ __host__ __device__ constexpr Trans trans(int a, uint32_t p)
 #define GB_K6 160
 #endif
 #ifndef GB_P1
-#define GB_P1 48
+#define GB_P1 56
 #endif
 constexpr int kK = GB_K6;        // unrolled candidates per class
 constexpr int kP1 = GB_P1;       // phase 1: candidates every word goes through
@@ -482,7 +482,7 @@ __device__ __forceinline__ void phase1(Lane6 &m0, Lane6 &m1, uint32_t *h, int la
 
 // ---- phase 1 with kW words per lane (words li, li + 32, ..., li + 32(kW-1)) ----
 #ifndef GB_W1
-#define GB_W1 4
+#define GB_W1 3
 #endif
 constexpr int kW = GB_W1;
 static_assert(kW * 32 * 32 < 65536, "16-bit packed per-warp counts");
