@@ -254,8 +254,20 @@ def main():
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     alu_peak = 148 * 64 * sm_mhz * 1e6 / 1e12           # T int32 lane-ops/s on the ALU pipe
     achieved = ops_per_even * evens_per_launch / avg_launch_s / 1e12
+    traffic, traffic_src = None, None
+    try:   # DRAM bytes per even n of verify_kernel from the latest committed ncu --set full capture
+        import glob
+        caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_verify_kernel_ncu.json")))
+        if caps:
+            cap = json.load(open(caps[-1]))
+            traffic = cap["dram_bytes_per_even"] * evens_per_launch
+            traffic_src = os.path.relpath(caps[-1], ROOT)
+    except Exception:
+        pass
     roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Tops/s",
-                "frac": achieved / alu_peak, "traffic": None,
+                "frac": achieved / alu_peak, "traffic": traffic,
+                "traffic_note": (f"DRAM read+write bytes per launch, scaled per even n from {traffic_src}"
+                                 if traffic_src else None),
                 "kernel": "verify_kernel (fused sieve + mark + fallback)",
                 "ops_per_even": ops_per_even,
                 "peak_basis": f"148 SM x 64 int32 lanes/clk (ALU pipe) x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
