@@ -94,7 +94,7 @@ uint32_t verify_tile_words(uint32_t halo)
     const uint32_t tw = (kVerifyDynSmemMax / 8 - halo - kWinSlackWords) & ~127u;   // multiple of 128 words
     return tw;
 }
-constexpr size_t kQueueBytes = (kThreads / 32) * 160 * 6;   // per-warp survivor queues (u32 U + u16 index)
+constexpr size_t kQueueBytes = (kThreads / 32) * 128 * 6;   // per-warp survivor queues (u32 U + u16 index)
 size_t verify_smem(uint32_t halo)
 {
     return 2 * 4ull * (halo + verify_tile_words(halo) + kWinSlackWords) + kQueueBytes;
@@ -379,6 +379,7 @@ gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_m
     a.med_idx = ctx->med_idx;
     a.med_off = ctx->med_off;
     a.i_b2 = count_le(ctx->h_primes, 16ull * (a.halo + a.tile_words));   // 2p > 32 (halo + tile) bits
+    a.i_b1 = count_le(ctx->h_primes, 32ull * (a.halo + a.tile_words));   // p > 32 (halo + tile) bits
     return launch_verify(a, grid, smem, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
 }
 

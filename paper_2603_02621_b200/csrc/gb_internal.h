@@ -75,6 +75,7 @@ struct VerifyArgs {
     const uint16_t *med_idx;  // LPT schedule of the medium primes over the CTA's warps
     const uint32_t *med_off;  // (kThreads/32 + 1 offsets)
     uint32_t i_b2;            // first prime index with 2p > a full window (<= 2 hits per class)
+    uint32_t i_b1;            // first prime index with p > a full window (<= 1 hit per class)
     uint32_t tile_words;      // words per class per tile: kTileWords, smaller when the halo is large
 };
 

@@ -58,7 +58,7 @@ __host__ __device__ constexpr Trans trans(int a, uint32_t p)
 constexpr int kK = GB_K6;        // unrolled candidates per class
 constexpr int kP1 = GB_P1;       // phase 1: candidates every word goes through
 constexpr uint32_t kWinSlack = 128;   // words past a window that phase-1 lanes may read (U = 0)
-constexpr int kQueue = 160;      // per-warp survivor queue (<= 31 carried + 32 kW per round)
+constexpr int kQueue = 128;      // per-warp survivor queue (<= 31 carried + 32 kW per round)
 static_assert(kK % 8 == 0 && kP1 % 8 == 0 && kP1 <= kK, "blocks of 8 candidates");
 
 
@@ -162,27 +162,31 @@ __device__ __forceinline__ void clear_bit(uint32_t w, uint32_t b)
     smem_and(w + ((b >> 5) << 2), clear_mask(b));
 }
 
-__device__ __forceinline__ void mark_progression(uint32_t w, uint32_t off, uint32_t p, uint32_t nw,
+__device__ __forceinline__ void mark_progression(uint32_t w, uint32_t off, uint32_t p, uint32_t hits,
                                                  uint32_t lane)
 {
-    // one warp, one prime: lane l marks bits off + l p + k 32p.  The stride is p
-    // whole words, so a lane's bit-in-word (hence its mask) never changes: only the
-    // word address moves, by 4p bytes per hit.
+    // one warp, one prime: lane l marks hits l, l + 32, ... (bits off + (l + 32i) p).
+    // The stride is p whole words, so a lane's bit-in-word (hence its mask) never
+    // changes: only the word address moves, by 4p bytes per hit.
+    const uint32_t n = (hits + 31 - lane) >> 5;         // this lane's hit count
+    if (n == 0) return;
     const uint32_t b0 = off + lane * p;
     const uint32_t mask = clear_mask(b0);
     const uint32_t step = 4 * p;
-    const uint32_t end = w + 4 * nw;
-    for (uint32_t ad = w + ((b0 >> 5) << 2); ad < end; ad += 4 * step) {   // 4 hits per trip, predicated
+    uint32_t ad = w + ((b0 >> 5) << 2);
+    uint32_t i = 0;
+    for (; i + 4 <= n; i += 4, ad += 4 * step) {
         smem_and(ad, mask);
-        if (ad + step < end) smem_and(ad + step, mask);
-        if (ad + 2 * step < end) smem_and(ad + 2 * step, mask);
-        if (ad + 3 * step < end) smem_and(ad + 3 * step, mask);
+        smem_and(ad + step, mask);
+        smem_and(ad + 2 * step, mask);
+        smem_and(ad + 3 * step, mask);
     }
+    for (; i < n; ++i, ad += step) smem_and(ad, mask);
 }
 
 template <bool DEF_TILE>
 __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
-                              Carry6 *cy, const MedSched &ms, uint32_t i_b2)
+                              Carry6 *cy, const MedSched &ms, uint32_t i_b2, uint32_t i_b1)
 {
     const int tid = threadIdx.x;
     const uint32_t lane = (uint32_t)tid & 31;
@@ -245,6 +249,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
     // handed out dynamically in ascending order (largest work first).
     const uint32_t m_end = sp.i_big < sp.n_use ? sp.i_big : sp.n_use;
     __shared__ uint32_t sh_mA[kMedMax], sh_mB[kMedMax];
+    __shared__ uint16_t sh_hA[kMedMax], sh_hB[kMedMax];     // hits per class in this window
     for (uint32_t pi = sp.i_med + tid; pi < m_end; pi += nt) {
         const uint4 k = __ldg(sp.pk + pi);        // p, kTileM mod p, rA, rB
         uint32_t oa = 0xFFFFFFFFu, ob = 0xFFFFFFFFu;
@@ -275,6 +280,8 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
         }
         sh_mA[pi - sp.i_med] = oa;
         sh_mB[pi - sp.i_med] = ob;
+        sh_hA[pi - sp.i_med] = (uint16_t)(oa < nbits ? (nbits - oa + k.x - 1) / k.x : 0);
+        sh_hB[pi - sp.i_med] = (uint16_t)(ob < nbits ? (nbits - ob + k.x - 1) / k.x : 0);
     }
     __syncthreads();
     // one warp per medium prime: the host's LPT schedule (longest work first onto
@@ -287,15 +294,18 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             const uint32_t pi = sp.i_med + rel;
             if (pi >= m_end) continue;
             const uint32_t p = __ldg(sp.primes + pi);
-            const uint32_t oa = sh_mA[rel], ob = sh_mB[rel];
-            if (oa < nbits) mark_progression(sA, oa, p, nw, lane);
-            if (ob < nbits) mark_progression(sB, ob, p, nw, lane);
+            mark_progression(sA, sh_mA[rel], p, sh_hA[rel], lane);
+            mark_progression(sB, sh_mB[rel], p, sh_hB[rel], lane);
         }
     }
     // large primes: one thread per prime.  Steady primes: kB in flight per thread.
     const uint32_t b_begin = sp.i_big > sp.i_med ? sp.i_big : sp.i_med;
     const uint32_t s_end = ns > b_begin ? (ns < sp.n_use ? ns : sp.n_use) : b_begin;
     const uint32_t b2 = i_b2 < b_begin ? b_begin : (i_b2 < s_end ? i_b2 : s_end);
+    const uint32_t b1 = i_b1 < b2 ? b2 : (i_b1 < s_end ? i_b1 : s_end);
+    uint32_t *__restrict__ cA = cy->off;                 // this CTA's carry row, class A
+    uint32_t *__restrict__ cB = cy->off + cy->stride;    // class B
+    const uint4 *__restrict__ pkp = sp.pk;
     constexpr int kB = 4;
     // steady primes with p <= full window / 2: hit loops (>= 2 hits per class)
     for (uint32_t w0 = b_begin + (tid & ~31u); w0 < b2; w0 += kB * nt) {   // warp-uniform trips
@@ -306,10 +316,10 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
         for (int k = 0; k < kB; ++k) {
             const uint32_t pi = p0 + k * nt;
             if (pi < b2) {
-                const uint4 q = __ldg(sp.pk + pi);
+                const uint4 q = __ldg(pkp + pi);
                 pt[k] = make_uint2(q.x, tile_mod<DEF_TILE>(cy, q));
-                oa[k] = cy->off[pi];
-                ob[k] = cy->off[cy->stride + pi];
+                oa[k] = __ldcg(cA + pi);
+                ob[k] = __ldcg(cB + pi);
             } else {
                 pt[k] = make_uint2(1, 0);
                 oa[k] = ob[k] = nbits;
@@ -322,43 +332,72 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             for (uint32_t b = ob[k]; b < nbits; b += p) clear_bit(sB, b);
             const uint32_t pi = p0 + k * nt;
             if (pi < b2) {
-                cy->off[pi] = oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm;
-                cy->off[cy->stride + pi] = ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm;
+                __stcg(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm);
+                __stcg(cB + pi, ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm);
             }
         }
         __syncwarp();   // reconverge: the per-lane hit loops diverge
     }
-    // steady primes with p > full window / 2: at most 2 hits per class, predicated,
-    // no loops and no divergence
+    // steady primes with window/2 < p <= window: at most 2 hits per class, predicated
     constexpr int kB2 = 8;
-    for (uint32_t w0 = b2 + (tid & ~31u); w0 < s_end; w0 += kB2 * nt) {
+    for (uint32_t w0 = b2 + (tid & ~31u); w0 < b1; w0 += kB2 * nt) {
         const uint32_t p0 = w0 + lane;
-        uint2 pt[kB2];
-        uint32_t oa[kB2], ob[kB2];
+        uint32_t pp[kB2], tt[kB2], oa[kB2], ob[kB2];
 #pragma unroll
         for (int k = 0; k < kB2; ++k) {
             const uint32_t pi = p0 + k * nt;
-            if (pi < s_end) {
-                const uint4 q = __ldg(sp.pk + pi);
-                pt[k] = make_uint2(q.x, tile_mod<DEF_TILE>(cy, q));
-                oa[k] = cy->off[pi];
-                ob[k] = cy->off[cy->stride + pi];
+            if (pi < b1) {
+                const uint4 q = __ldg(pkp + pi);
+                pp[k] = q.x;
+                tt[k] = tile_mod<DEF_TILE>(cy, q);
+                oa[k] = __ldcg(cA + pi);
+                ob[k] = __ldcg(cB + pi);
             } else {
-                pt[k] = make_uint2(nbits, 0);
+                pp[k] = nbits; tt[k] = 0;
                 oa[k] = ob[k] = nbits;
             }
         }
 #pragma unroll
         for (int k = 0; k < kB2; ++k) {
-            const uint32_t p = pt[k].x, tm = pt[k].y;
+            const uint32_t p = pp[k], tm = tt[k];
             if (oa[k] < nbits) clear_bit(sA, oa[k]);
             if (oa[k] + p < nbits) clear_bit(sA, oa[k] + p);
             if (ob[k] < nbits) clear_bit(sB, ob[k]);
             if (ob[k] + p < nbits) clear_bit(sB, ob[k] + p);
             const uint32_t pi = p0 + k * nt;
+            if (pi < b1) {
+                __stcg(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm);
+                __stcg(cB + pi, ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm);
+            }
+        }
+    }
+    // steady primes with p > a full window: at most 1 hit per class
+    for (uint32_t w0 = b1 + (tid & ~31u); w0 < s_end; w0 += kB2 * nt) {
+        const uint32_t p0 = w0 + lane;
+        uint32_t pp[kB2], tt[kB2], oa[kB2], ob[kB2];
+#pragma unroll
+        for (int k = 0; k < kB2; ++k) {
+            const uint32_t pi = p0 + k * nt;
             if (pi < s_end) {
-                cy->off[pi] = oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm;
-                cy->off[cy->stride + pi] = ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm;
+                const uint4 q = __ldg(pkp + pi);
+                pp[k] = q.x;
+                tt[k] = tile_mod<DEF_TILE>(cy, q);
+                oa[k] = __ldcg(cA + pi);
+                ob[k] = __ldcg(cB + pi);
+            } else {
+                pp[k] = nbits; tt[k] = 0;
+                oa[k] = ob[k] = nbits;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kB2; ++k) {
+            const uint32_t p = pp[k], tm = tt[k];
+            if (oa[k] < nbits) clear_bit(sA, oa[k]);
+            if (ob[k] < nbits) clear_bit(sB, ob[k]);
+            const uint32_t pi = p0 + k * nt;
+            if (pi < s_end) {
+                __stcg(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm);
+                __stcg(cB + pi, ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm);
             }
         }
     }
@@ -486,6 +525,7 @@ __device__ __forceinline__ void phase1(Lane6 &m0, Lane6 &m1, uint32_t *h, int la
 #endif
 constexpr int kW = GB_W1;
 static_assert(kW * 32 * 32 < 65536, "16-bit packed per-warp counts");
+static_assert(31 + 32 * kW <= kQueue, "survivor queue capacity");
 
 struct LaneQ {
     const uint32_t *wa, *wb;   // class A / B window words aligned with word 0 (word k at +32k)
@@ -936,9 +976,9 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
 #endif
         cy.n_steady = sh.ns;
         if (cy.tile_m == kTileM)
-            sieve6_window<true>(wA, wB, g0, halo + tw, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2);
+            sieve6_window<true>(wA, wB, g0, halo + tw, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2, a.i_b1);
         else
-            sieve6_window<false>(wA, wB, g0, halo + tw, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2);
+            sieve6_window<false>(wA, wB, g0, halo + tw, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2, a.i_b1);
         cy.have_prev = true;
 #ifdef GB_PROFILE_PHASES
         const long long t1 = clock64();
