@@ -49,8 +49,8 @@ def test_workspace_planning():
     assert gb.gb_ctx_workspace_bytes(10**12 + 1, 2) == 0          # p_max < 3
     assert gb.gb_ctx_workspace_bytes(4, 65521) == 0                 # empty
     assert gb.gb_ctx_workspace_bytes(10**12 + 1, gb.PMAX_LIMIT + 1) == 0
-    # 4e18 window: base primes to 2e9 fit in a few GB
-    assert gb.gb_ctx_workspace_bytes(4 * 10**18, 65521) < 4 * 2**30
+    # 4e18 window: 98M base primes (list, reciprocals, wheel constants) fit in a few GB
+    assert gb.gb_ctx_workspace_bytes(4 * 10**18, 65521) < 8 * 2**30
     assert gb.gb_status_string(gb.GB_ERANGE).startswith("GB_ERANGE")
 
 
