@@ -38,6 +38,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--N", type=float, default=1e12)
+    ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
+                    help="c4: every even n in [4, N] (the metric's workload); c5: the window "
+                         "[4e18 - 1e11, 4e18) of BASELINE.json configs[4]")
     ap.add_argument("--p-max", type=int, default=65521)
     ap.add_argument("--strips-per-rank", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -88,20 +91,29 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- CPU oracle legs
-def oracle_sample(N: int, target_s: float):
-    """Time the CPU oracle (as it stands) on a top slice of [4, N], doubling the
+def workload(args):
+    """(lo, hi, origin, description, algorithmic int32 ops per even n) of the run."""
+    if args.workload == "c5":
+        top = 4 * 10**18
+        return top - 10**11, top, top - 10**11, "C5 window: every even n in [4e18 - 1e11, 4e18)", C5_OPS_PER_EVEN
+    N = int(args.N)
+    return 4, N + 1, 0, f"N={N:.0e} exhaustive verification, even n in [4, N]", ALU_OPS_PER_EVEN
+
+
+def oracle_sample(hi: int, target_s: float, lo_min: int = 4):
+    """Time the CPU oracle (as it stands) on a top slice of [lo_min, hi), growing the
     slice until it has run for at least target_s seconds."""
     from oracle import oracle
     threads = oracle.default_threads()
     span = 1 << 27
     while True:
-        lo = max(4, N + 1 - span)
+        lo = max(lo_min, hi - span)
         t0 = time.perf_counter()
-        r, _ = oracle.verify(lo, N + 1, threads=threads)
+        r, _ = oracle.verify(lo, hi, threads=threads)
         dt = time.perf_counter() - t0
-        if dt >= target_s or lo == 4:
+        if dt >= target_s or lo == lo_min:
             return {"value": r["evens"] / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
-                    "sample": f"even n in [{lo}, {N}] ({r['evens']} evens, {dt:.2f} s, top of the range)",
+                    "sample": f"even n in [{lo}, {hi}) ({r['evens']} evens, {dt:.2f} s, top of the range)",
                     "seconds": dt, "evens": r["evens"]}
         span = int(span * min(8.0, max(2.0, 1.2 * target_s / max(dt, 1e-3))))
 
@@ -109,14 +121,14 @@ def oracle_sample(N: int, target_s: float):
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
-    N = int(args.N)
+    lo, hi, _, desc, _ = workload(args)
     per_step = max(1.0, args.cpu_seconds / 4)
     for _ in range(args.warmup):
-        oracle_sample(N, per_step / 4)
+        oracle_sample(hi, per_step / 4, lo)
     vals, times, evens = [], [], 0
-    first = oracle_sample(N, per_step)
+    first = oracle_sample(hi, per_step, lo)
     for i in range(args.steps):
-        s = first if i == 0 else oracle_sample(N, per_step)
+        s = first if i == 0 else oracle_sample(hi, per_step, lo)
         vals.append(s["value"])
         times.append(s["seconds"])
         evens += s["evens"]
@@ -125,10 +137,9 @@ def run_reference(args, rank: int, world: int):
             "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (deterministic number-theoretic range)", "impl": "reference",
-            "config": {"workload": f"N={N:.0e} exhaustive verification, even n in [4, N]", "N": N,
-                       "sample": first["sample"]},
+            "config": {"workload": desc, "lo": lo, "hi": hi, "sample": first["sample"]},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": first["cores"], "kind": "oracle",
-                             "sample": f"{args.steps} top-of-range slices of [4, {N}], ~{per_step:.1f} s each"},
+                             "sample": f"{args.steps} top-of-range slices of [{lo}, {hi}), ~{per_step:.1f} s each"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -157,11 +168,10 @@ def main():
     from paper_2603_02621_b200 import dist as gdist
     from paper_2603_02621_b200.verifier import Verifier
 
-    N = int(args.N)
-    lo, hi = 4, N + 1
+    lo, hi, origin, desc, ops_per_even = workload(args)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-    V = Verifier(hi_max=hi, p_max=args.p_max, device=local, stream=stream)
+    V = Verifier(hi_max=hi, p_max=args.p_max, origin=origin, device=local, stream=stream)
     strips = gdist.rank_strips(gdist.plan_strips(lo, hi, args.strips_per_rank * world), rank, world)
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(4 * l2_bytes, 1 << 28) // 4, dtype=torch.int32, device=dev)
@@ -212,7 +222,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     box_ms, box_kern_ms = float(t[0]), float(t[1])
-    res = gb.decode_result(results[-1][2].cpu())
+    res = V.decode(results[-1][2])
     evens = res["evens"]
     value = evens * args.steps / (box_ms / 1e3)
 
@@ -250,7 +260,6 @@ def main():
     n_launch = len(kern_ms)
     avg_launch_s = (sum(kern_ms) / n_launch) / 1e3 if n_launch else float("nan")
     evens_per_launch = evens / max(1, len(strips) * world)
-    ops_per_even = ALU_OPS_PER_EVEN
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     alu_peak = 148 * 64 * sm_mhz * 1e6 / 1e12           # T int32 lane-ops/s on the ALU pipe
     achieved = ops_per_even * evens_per_launch / avg_launch_s / 1e12
@@ -276,7 +285,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_sample(N, args.cpu_seconds)
+        cpu = oracle_sample(hi, args.cpu_seconds, lo)
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
@@ -284,8 +293,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": box_ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "u64",
                 "data": "synthetic (deterministic number-theoretic range; no dataset)",
-                "config": {"workload": f"N={N:.0e} exhaustive verification, even n in [4, N]",
-                           "N": N, "p_max": args.p_max, "strips_per_rank": args.strips_per_rank,
+                "config": {"workload": desc, "lo": lo, "hi": hi, "p_max": args.p_max, "strips_per_rank": args.strips_per_rank,
                            "parallelism": f"range-sharded x{world}", "l2": "flushed between steps"},
                 "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "roofline": roofline,
                 "cpu_baseline": cpu,
@@ -304,6 +312,8 @@ def main():
 #   mark  : 1.01 64-bit word-iterations per even n (64-even exit) x 6 int32 ops
 #           (2 funnel shifts, 2 AND, 2 XOR)
 ALU_OPS_PER_EVEN = 2.387 + 1.01 * 6
+# the same yardstick in the C5 window ("4e18 window" row)
+C5_OPS_PER_EVEN = 2.826 + 1.63 * 6
 
 if __name__ == "__main__":
     main()

@@ -31,8 +31,8 @@ uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 constexpr uint64_t kMaxSms = 160;   // workspace sizing bound (B200: 148)
 
 struct Layout {
-    uint64_t R, bits_words, list_cap, n_blk, carry_stride, carry_ctas;
-    uint64_t off_bits, off_primes, off_magic, off_tmod, off_carry, off_sched, off_blk, off_counter,
+    uint64_t R, bits_words, list_cap, n_blk, carry_stride, carry_ctas, lmask_stride;
+    uint64_t off_bits, off_primes, off_magic, off_tmod, off_carry, off_lmask, off_sched, off_blk, off_counter,
         off_res, off_dump, total;
 };
 
@@ -42,6 +42,8 @@ uint64_t pi_upper(uint64_t x)
     if (x < 17) return 8;
     return (uint64_t)(1.25506 * (double)x / __builtin_log((double)x)) + 64;
 }
+
+uint32_t verify_halo(uint32_t p_top);
 
 bool plan(uint64_t hi_max, uint32_t p_max, Layout &L)
 {
@@ -58,6 +60,11 @@ bool plan(uint64_t hi_max, uint32_t p_max, Layout &L)
     const uint64_t sq = isqrt_u64(hi_max - 1);
     L.carry_stride = align_up(pi_upper(std::min<uint64_t>(sq, kCarryPrimeMax)), 64);
     L.carry_ctas = 0;   // filled by the caller with the device's SM count
+    // K-LARGE chunk mask (two wheel classes), only when some sieving prime exceeds
+    // the carried range: kLargeTilesPerSm tiles per SM + the largest halo
+    L.lmask_stride = sq > kCarryPrimeMax
+                         ? align_up((uint64_t)kLargeTilesPerSm * kMaxSms * kTileWords + verify_halo(p_max) + 64, 64)
+                         : 0;
     L.n_blk = (L.bits_words + kScanBlockWords - 1) / kScanBlockWords;
     uint64_t o = 0;
     L.off_bits = o;    o = align_up(o + 8 * L.bits_words, 256);
@@ -65,6 +72,7 @@ bool plan(uint64_t hi_max, uint32_t p_max, Layout &L)
     L.off_magic = o;   o = align_up(o + 8 * L.list_cap, 256);
     L.off_tmod = o;    o = align_up(o + 16 * L.list_cap, 256);
     L.off_carry = o;   o = align_up(o + 8 * L.carry_stride * (uint64_t)kMaxBlocksPerSm * kMaxSms, 256);
+    L.off_lmask = o;   o = align_up(o + 8 * L.lmask_stride, 256);
     L.off_sched = o;   o = align_up(o + 2 * 1024 + 4 * (kThreads / 32 + 1), 256);
     L.off_blk = o;     o = align_up(o + 8 * (L.n_blk + 1), 256);
     L.off_counter = o; o = align_up(o + 256, 256);
@@ -175,6 +183,8 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
     c->pk = (uint4 *)(ws + L.off_tmod);
     c->carry = (uint32_t *)(ws + L.off_carry);
     c->carry_stride = L.carry_stride;
+    c->lmask = L.lmask_stride ? (uint32_t *)(ws + L.off_lmask) : nullptr;
+    c->lmask_stride = L.lmask_stride;
     c->med_idx = (uint16_t *)(ws + L.off_sched);
     c->med_off = (uint32_t *)(ws + L.off_sched + 2 * 1024);
     c->blk = (uint64_t *)(ws + L.off_blk);
@@ -380,7 +390,44 @@ gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_m
     a.med_off = ctx->med_off;
     a.i_b2 = count_le(ctx->h_primes, 16ull * (a.halo + a.tile_words));   // 2p > 32 (halo + tile) bits
     a.i_b1 = count_le(ctx->h_primes, 32ull * (a.halo + a.tile_words));   // p > 32 (halo + tile) bits
-    return launch_verify(a, grid, smem, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
+    a.lmask = nullptr;
+    a.lmask_g0 = 0;
+    a.lmask_stride = 0;
+    const uint32_t i_large = count_le(ctx->h_primes, kCarryPrimeMax);
+    if (a.sp.n_use <= i_large)
+        return launch_verify(a, grid, smem, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
+    // Sieving primes above kCarryPrimeMax: chunks of whole tiles (a multiple of the
+    // grid), each preceded by K-LARGE over its windows (tiles + the halo below).
+    if (!ctx->lmask) return GB_EINTERNAL;
+    const uint32_t n_use_all = a.sp.n_use;
+    a.sp.n_use = i_large;
+    const uint64_t cap_tiles = (ctx->lmask_stride - a.halo - 64) / a.tile_words;
+    uint64_t chunk_tiles = std::min<uint64_t>(cap_tiles, (uint64_t)kLargeTilesPerSm * grid);
+    if (chunk_tiles > (uint64_t)grid) chunk_tiles -= chunk_tiles % (uint64_t)grid;
+    if (chunk_tiles == 0) return GB_EINTERNAL;
+    for (uint64_t t0 = 0; t0 < a.n_tiles; t0 += chunk_tiles) {
+        VerifyArgs b = a;
+        const uint64_t nt = std::min<uint64_t>(chunk_tiles, a.n_tiles - t0);
+        b.u_first = a.u_first + t0 * a.tile_words;
+        b.u_end = std::min<uint64_t>(a.u_end, b.u_first + nt * a.tile_words);
+        b.n_tiles = nt;
+        LargeArgs L;
+        L.primes = ctx->primes;
+        L.magic = ctx->magic;
+        L.i_begin = i_large;
+        L.i_end = n_use_all;
+        L.g0 = (int64_t)b.u_first - (int64_t)a.halo;
+        L.nw = (uint32_t)(b.u_end - b.u_first + a.halo);
+        L.stride = ctx->lmask_stride;
+        L.mask = ctx->lmask;
+        b.lmask = ctx->lmask;
+        b.lmask_g0 = L.g0;
+        b.lmask_stride = L.stride;
+        if (launch_large(L, ctx->num_sms, S(stream)) != cudaSuccess) return GB_ECUDA;
+        const int gb = (int)std::min<uint64_t>((uint64_t)grid, nt);
+        if (launch_verify(b, gb, smem, S(stream)) != cudaSuccess) return GB_ECUDA;
+    }
+    return GB_OK;
 }
 
 gb_status gb_verify_range(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_max, int64_t *d_result,

@@ -31,6 +31,13 @@ constexpr uint64_t kDumpScratch = 1ull << 24;  // u32 entries of host-API dump s
 constexpr int kScanBlockWords = 2048;      // u64 words per K-BASE compaction block
 constexpr uint32_t kCarryPrimeMax = 1u << 21;  // verify CTAs carry sieve offsets of primes below
 constexpr int kMaxBlocksPerSm = 4;         // sizing bound for per-CTA carry storage
+#ifndef GB_LARGE_TILES_PER_SM
+#define GB_LARGE_TILES_PER_SM 3
+#endif
+// Ranges that need sieving primes above kCarryPrimeMax (hi > 2^42, e.g. the 4e18
+// window) run in chunks of GB_LARGE_TILES_PER_SM verify tiles per SM; before each
+// chunk K-LARGE marks the multiples of those primes into an L2-resident wheel mask.
+constexpr int kLargeTilesPerSm = GB_LARGE_TILES_PER_SM;
 
 // Arguments of the window sieve (K-SIEVE) shared by every caller.
 struct SievePrimes {
@@ -40,6 +47,19 @@ struct SievePrimes {
     uint32_t i_med;           // first index with p > 31 (word patterns below)
     uint32_t i_big;           // first index with p > kWarpPrimeMax
     uint32_t n_use;           // primes usable (p^2 beyond the window are skipped)
+};
+
+// K-LARGE: multiples of primes [i_begin, i_end) cleared in a wheel-class mask of
+// nw words per class (class A at mask[0..nw), class B at mask[stride..stride+nw)),
+// word i <-> m in [32(g0+i), 32(g0+i)+32); every other bit stays 1.
+struct LargeArgs {
+    const uint32_t *primes;
+    const uint64_t *magic;
+    uint32_t i_begin, i_end;
+    int64_t g0;
+    uint32_t nw;
+    uint64_t stride;
+    uint32_t *mask;
 };
 
 struct SegmentArgs {
@@ -77,6 +97,9 @@ struct VerifyArgs {
     uint32_t i_b2;            // first prime index with 2p > a full window (<= 2 hits per class)
     uint32_t i_b1;            // first prime index with p > a full window (<= 1 hit per class)
     uint32_t tile_words;      // words per class per tile: kTileWords, smaller when the halo is large
+    const uint32_t *lmask;    // K-LARGE mask of this chunk (nullable): ANDed into every window
+    int64_t lmask_g0;         // g of mask word 0
+    uint64_t lmask_stride;    // class B words start here
 };
 
 // Launchers (gb_kernels.cu).  Each returns the cudaGetLastError() of its launch.
@@ -91,6 +114,7 @@ cudaError_t launch_scatter(const uint64_t *bits, uint64_t n_words, const uint64_
 cudaError_t launch_result_init(int64_t *res, cudaStream_t st);
 cudaError_t launch_result_finalize(int64_t *res, cudaStream_t st);
 cudaError_t launch_verify(const VerifyArgs &a, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_large(const LargeArgs &a, int num_sms, cudaStream_t st);   // mask fill + marking
 cudaError_t launch_is_prime(const uint64_t *x, uint8_t *out, uint64_t n, const uint64_t *bits,
                             uint64_t R, cudaStream_t st);
 cudaError_t configure_verify(size_t smem_max);
@@ -114,6 +138,8 @@ struct gb_ctx {
     uint64_t *magic;
     uint4 *pk;             // (p, kTileM mod p, rA, rB)
     uint32_t *carry;       // verify-kernel carried offsets: carry_ctas x carry_stride
+    uint32_t *lmask;       // K-LARGE chunk mask (null when hi_max needs no primes > kCarryPrimeMax)
+    uint64_t lmask_stride; // u32 words per class
     uint64_t carry_stride;
     uint32_t carry_ctas;
     uint16_t *med_idx;     // LPT schedule of medium primes (host-computed, copied once)

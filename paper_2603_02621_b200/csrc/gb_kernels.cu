@@ -12,6 +12,7 @@
 // 64-bit word of the paper's layout is two consecutive 32-bit words, little-endian).
 #include <stdint.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 
@@ -259,6 +260,54 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint64_t *bits, uint
 }
 
 // ---------------------------------------------------------------------------
+// K-LARGE: sieving primes too large for the per-tile shared-memory sieve (p >
+// kCarryPrimeMax: at most a few hits per verify window, most windows none).  Their
+// multiples in class A (6m+1) and class B (6m+5) are cleared, one thread per prime,
+// by no-return L2 atomics into a chunk mask that stays resident in L2; the verify
+// kernel ANDs the mask into its windows.  The prime table is streamed with
+// evict-first loads so it does not push the mask out of L2.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) large_fill_kernel(uint32_t *mask, uint64_t stride, uint32_t nw)
+{
+    const uint64_t n = stride + nw;             // class A [0, nw) .. class B [stride, stride + nw)
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        mask[i] = 0xFFFFFFFFu;
+}
+
+__device__ __forceinline__ void gmem_and(uint32_t *p, uint32_t v)
+{
+    asm volatile("red.global.and.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(256) large_mark_kernel(LargeArgs a)
+{
+    const int64_t m_lo = a.g0 * 32;
+    const int64_t m_hi = m_lo + 32 * (int64_t)a.nw;
+    const uint32_t nbits = 32 * a.nw;
+    const uint64_t n = a.i_end - a.i_begin;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t pi = a.i_begin + (uint32_t)k;
+        const uint32_t p = __ldcs(a.primes + pi);
+        // the first multiple cleared is p^2 (= 6m + 1, class A): p itself stays set
+        const int64_t mmin = (int64_t)(((uint64_t)p * p - 1) / 6);
+        if (mmin >= m_hi) continue;
+        const uint64_t ms = (uint64_t)(mmin > m_lo ? mmin : m_lo);
+        const uint32_t rem = mod_magic(ms, p, __ldcs(a.magic + pi));
+        // m with p | 6m+1: m == -1/6 (mod p); p | 6m+5: m == -5/6 (mod p)
+        const uint64_t inv6 = (p % 6 == 1) ? (5ull * p + 1) / 6 : ((uint64_t)p + 1) / 6;
+        const uint32_t rA = p - (uint32_t)inv6;
+        uint64_t t = 5ull * rA;
+        while (t >= p) t -= p;
+        const uint32_t rB = (uint32_t)t;
+        const uint64_t base = ms - (uint64_t)m_lo;
+        uint64_t bA = base + (rA >= rem ? rA - rem : rA + p - rem);
+        uint64_t bB = base + (rB >= rem ? rB - rem : rB + p - rem);
+        for (; bA < nbits; bA += p) gmem_and(a.mask + (bA >> 5), clear_mask((uint32_t)bA));
+        for (; bB < nbits; bB += p) gmem_and(a.mask + a.stride + (bB >> 5), clear_mask((uint32_t)bB));
+    }
+}
+
+// ---------------------------------------------------------------------------
 // result vector
 // ---------------------------------------------------------------------------
 __global__ void result_init_kernel(int64_t *r)
@@ -330,6 +379,19 @@ cudaError_t launch_scatter(const uint64_t *bits, uint64_t n_words, const uint64_
 {
     const uint64_t nb = (n_words + kScanBlockWords - 1) / kScanBlockWords;
     scatter_kernel<<<(unsigned)nb, 256, 0, st>>>(bits, n_words, blk, primes, magic, pk);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_large(const LargeArgs &a, int num_sms, cudaStream_t st)
+{
+    large_fill_kernel<<<(unsigned)(8 * num_sms), 256, 0, st>>>(a.mask, a.stride, a.nw);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || a.i_end <= a.i_begin) return e;
+    const uint64_t n = a.i_end - a.i_begin;
+    const uint64_t nb = std::min<uint64_t>((n + 255) / 256, 64ull * num_sms);
+    large_mark_kernel<<<(unsigned)nb, 256, 0, st>>>(a);
     count_launch();
     return cudaGetLastError();
 }

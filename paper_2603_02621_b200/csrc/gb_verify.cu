@@ -186,7 +186,8 @@ __device__ __forceinline__ void mark_progression(uint32_t w, uint32_t off, uint3
 
 template <bool DEF_TILE>
 __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
-                              Carry6 *cy, const MedSched &ms, uint32_t i_b2, uint32_t i_b1)
+                              Carry6 *cy, const MedSched &ms, uint32_t i_b2, uint32_t i_b1,
+                              const uint32_t *__restrict__ lm, int64_t lg0, uint64_t lstride)
 {
     const int tid = threadIdx.x;
     const uint32_t lane = (uint32_t)tid & 31;
@@ -219,6 +220,10 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
                     // B (6m+5): 5, 11, 17, 23, 29 at m = 0..4; and 1 = 6*0+1 is not prime
                     va = (va | 0x2Eu) & ~1u;
                     vb |= 0x1Fu;
+                }
+                if (lm) {   // K-LARGE mask of this chunk (primes above the carried range)
+                    va &= __ldcg(lm + (g - lg0));
+                    vb &= __ldcg(lm + lstride + (g - lg0));
                 }
             }
             wA[i] = va;
@@ -976,9 +981,11 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
 #endif
         cy.n_steady = sh.ns;
         if (cy.tile_m == kTileM)
-            sieve6_window<true>(wA, wB, g0, halo + tw, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2, a.i_b1);
+            sieve6_window<true>(wA, wB, g0, halo + tw, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2, a.i_b1,
+                                a.lmask, a.lmask_g0, a.lmask_stride);
         else
-            sieve6_window<false>(wA, wB, g0, halo + tw, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2, a.i_b1);
+            sieve6_window<false>(wA, wB, g0, halo + tw, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2, a.i_b1,
+                                 a.lmask, a.lmask_g0, a.lmask_stride);
         cy.have_prev = true;
 #ifdef GB_PROFILE_PHASES
         const long long t1 = clock64();

@@ -30,6 +30,16 @@ for w in $what; do
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:verify_kernel -c 1 \
         -f -o gpurun_out/prof python scripts/prof_one.py --span 36 > gpurun_out/prof.log 2>&1
       echo "ncu full rc=$?"; tail -2 gpurun_out/prof.log ;;
+    t4e18)
+      timeout 1200 python -m pytest tests/test_gpu_4e18.py -x -q > gpurun_out/gpu_tests_4e18.log 2>&1
+      echo "4e18 tests rc=$?"; tail -3 gpurun_out/gpu_tests_4e18.log ;;
+    c5)
+      timeout 900 python bench.py --workload c5 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
+      echo "bench c5 rc=$?"; cat gpurun_out/bench_c5.json; tail -3 gpurun_out/bench_c5.err
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
+        --log-file gpurun_out/launches_c5.csv python bench.py --workload c5 --steps 1 --warmup 1 --no-cpu-baseline \
+        > gpurun_out/bench_c5_under_ncu.log 2>&1
+      echo "ncu c5 launches rc=$?" ;;
     time)
       timeout 600 python scripts/prof_one.py --span 36 --time 10 2>&1 | tail -2 ;;
   esac

@@ -254,3 +254,20 @@ def test_golden_1e12_closed_forms():
     assert g["hist"]["2"] == PUB["pi"]["1000000000000"] - 1 == 37607912017
     assert g["hist"]["3"] == PUB["pi"]["1000000000000"] - 1 - PUB["pi2"]["1000000000000"] == 35737326797
     assert g["unresolved"] == 0 and g["fastpath_unresolved"] == 0
+
+
+def test_golden_4e18_windows_match_appendix():
+    """The oracle-written C5 window goldens agree with SURVEY.md Appendix A's
+    independent (12-base MR, no sieve) window maxima: 3,191 @ 3,999,999,999,998,238,538
+    at the top of [4e18 - 1e11, 4e18) and 3,167 @ 3,999,999,900,003,045,538 at its
+    bottom; every window is fully verified with no fallback."""
+    path = os.path.join(GOLDEN, "verify_4e18_windows.json")
+    doc = json.load(open(path))
+    w = {(x["lo"], x["hi"]): x["result"] for x in doc["windows"]}
+    top = w[(4 * 10**18 - 2**23, 4 * 10**18)]
+    bot = w[(4 * 10**18 - 10**11, 4 * 10**18 - 10**11 + 2**23)]
+    assert (top["max_pmin"], top["max_pmin_n"]) == (3191, 3999999999998238538)
+    assert (bot["max_pmin"], bot["max_pmin_n"]) == (3167, 3999999900003045538)
+    for r in w.values():
+        assert r["evens"] == r["verified"] and r["fastpath_unresolved"] == 0 and r["unresolved"] == 0
+        assert sum(r["hist"].values()) == r["evens"]
