@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--strips-per-rank", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sieve", action="store_true", help="skip the standalone sieve GB/s leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -283,6 +284,36 @@ def main():
                 "kernel_ms_per_launch": avg_launch_s * 1e3, "launches_timed": n_launch,
                 "kernel_share_of_step": box_kern_ms / box_ms if box_ms else None}
 
+    # ---- sieve GB/s (BASELINE.json metric, second half): standalone gb_sieve_segment
+    # (K-SIEVE, the paper's odd-only layout PAPER.md:46-51) writing the bitset of the
+    # top 2^34 integers of the range to HBM; bytes written / device time
+    sieve = None
+    if not args.no_sieve:
+        nwords = 1 << 27                                   # u64 words = 2^34 integers, 1 GiB
+        w_hi = (hi - 3) // 128
+        w_lo = max(0, w_hi - nwords)
+        out = torch.empty(w_hi - w_lo, dtype=torch.int64, device=dev)
+        for _ in range(2):
+            gb.gb_sieve_segment(V.ctx, w_lo, w_hi - w_lo, out, stream)
+        ev = []
+        for _ in range(5):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            gb.gb_sieve_segment(V.ctx, w_lo, w_hi - w_lo, out, stream)
+            e1.record(stream)
+            ev.append((e0, e1))
+        torch.cuda.synchronize()
+        ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+        nbytes = 8 * (w_hi - w_lo)
+        hbm = peaks.get("hbm_gbs") or 6545.9
+        sieve = {"value": nbytes / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_launch": ms,
+                 "odd_integers_per_s": 64 * (w_hi - w_lo) / (ms / 1e3),
+                 "window": f"odd q in [{3 + 128 * w_lo}, {3 + 128 * w_hi})",
+                 "kernel": "segment_kernel (gb_sieve_segment)",
+                 "hbm_frac": nbytes / (ms / 1e3) / 1e9 / hbm, "hbm_peak_gbps": hbm}
+        del out
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_sample(hi, args.cpu_seconds, lo)
@@ -296,7 +327,7 @@ def main():
                 "config": {"workload": desc, "lo": lo, "hi": hi, "p_max": args.p_max, "strips_per_rank": args.strips_per_rank,
                            "parallelism": f"range-sharded x{world}", "l2": "flushed between steps"},
                 "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "roofline": roofline,
-                "cpu_baseline": cpu,
+                "cpu_baseline": cpu, "sieve": sieve,
                 "result": {k: res[k] for k in ("evens", "verified", "fastpath_unresolved", "unresolved",
                                                   "max_pmin", "max_pmin_n", "sum_pmin", "chk")},
                 "step_ms": step_ms}

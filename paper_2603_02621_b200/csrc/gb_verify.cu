@@ -916,7 +916,15 @@ __device__ __forceinline__ void flush_queue(int cls, Shared6 &sh, uint32_t &qn, 
 
 // UNROLL: every unrolled candidate of the three class tables is <= p_max.
 template <bool DUMP, bool UNROLL>
-__global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a)
+// __grid_constant__: the cold out-of-line paths take `a` by reference; without it
+// the whole parameter block is copied to the local-memory stack and every field
+// read becomes a local load (long-scoreboard stalls in the hot loop).
+#ifdef GB_NO_GRIDCONST
+#define GB_PARAM VerifyArgs a
+#else
+#define GB_PARAM const __grid_constant__ VerifyArgs a
+#endif
+__global__ void __launch_bounds__(kThreads) verify_kernel(GB_PARAM)
 {
     uint32_t *win = g_win;                     // class A window | class B window | queues
     __shared__ Shared6 sh;
