@@ -267,43 +267,145 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint64_t *bits, uint
 // kernel ANDs the mask into its windows.  The prime table is streamed with
 // evict-first loads so it does not push the mask out of L2.
 // ---------------------------------------------------------------------------
+#ifndef GB_LARGE_NOHINT
+#define GB_LARGE_HINT 1
+#else
+#define GB_LARGE_HINT 0
+#endif
+// L2 policy for the chunk mask: keep it resident (evict_last) while the prime table
+// streams through with evict-first loads
+__device__ __forceinline__ uint64_t l2_keep_policy()
+{
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
 __global__ void __launch_bounds__(256) large_fill_kernel(uint32_t *mask, uint64_t stride, uint32_t nw)
 {
     const uint64_t n = stride + nw;             // class A [0, nw) .. class B [stride, stride + nw)
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+#if GB_LARGE_HINT
+    const uint64_t pol = l2_keep_policy();
+#endif
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+#if GB_LARGE_HINT
+        asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(mask + i), "r"(0xFFFFFFFFu), "l"(pol)
+                     : "memory");
+#else
         mask[i] = 0xFFFFFFFFu;
+#endif
+    }
 }
 
-__device__ __forceinline__ void gmem_and(uint32_t *p, uint32_t v)
+__device__ __forceinline__ void gmem_and(uint32_t *p, uint32_t v, uint64_t pol)
 {
+#if GB_LARGE_HINT
+    asm volatile("red.global.and.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+#else
     asm volatile("red.global.and.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#endif
 }
 
-__global__ void __launch_bounds__(256) large_mark_kernel(LargeArgs a)
+#ifndef GB_LARGE_ILP
+#define GB_LARGE_ILP 2
+#endif
+#ifndef GB_LARGE_BLOCK
+#define GB_LARGE_BLOCK 256
+#endif
+#ifndef GB_LARGE_GRID_PER_SM
+#define GB_LARGE_GRID_PER_SM 64
+#endif
+constexpr int kLargeIlp = GB_LARGE_ILP;        // primes in flight per thread
+constexpr int kLargeBlock = GB_LARGE_BLOCK;
+
+// first hits (bits relative to the mask start) of prime p in class A and class B,
+// or >= nbits; the masks are < 2^30 bits, so offsets are 32-bit
+// x mod p through a double-precision quotient estimate, within a few units of the
+// true quotient while x / p < 2^45 (K-LARGE: x < 2^60, p > 2^21); an A/B option
+// (GB_LARGE_FP64MOD) that drops the reciprocal-table reads -- measured no faster
+__device__ __forceinline__ uint32_t mod_fp64(uint64_t x, uint32_t p)
+{
+    const int64_t q = (int64_t)__dmul_rn((double)x, __drcp_rn((double)p));
+    int64_t r = (int64_t)(x - (uint64_t)q * p);
+    while (r < 0) r += p;
+    while (r >= (int64_t)p) r -= p;
+    return (uint32_t)r;
+}
+
+__device__ __forceinline__ void large_first_hits(uint32_t p, const uint64_t *magic_ptr, int64_t m_lo, int64_t m_hi,
+                                                 uint32_t nbits, uint32_t &bA, uint32_t &bB)
+{
+    bA = bB = nbits;
+    // the first multiple cleared is p^2 (= 6m + 1, class A): p itself stays set
+    const int64_t mmin = (int64_t)(((uint64_t)p * p - 1) / 6);
+    if (mmin >= m_hi) return;
+    const uint64_t ms = (uint64_t)(mmin > m_lo ? mmin : m_lo);
+#ifdef GB_LARGE_FP64MOD
+    (void)magic_ptr;
+    const uint32_t rem = mod_fp64(ms, p);
+#else
+    const uint32_t rem = mod_magic(ms, p, __ldcs(magic_ptr));
+#endif
+    // m with p | 6m+1: m == -1/6 (mod p); p | 6m+5: m == -5/6 (mod p)
+    const uint64_t inv6 = (p % 6 == 1) ? (5ull * p + 1) / 6 : ((uint64_t)p + 1) / 6;
+    const uint32_t rA = p - (uint32_t)inv6;
+    uint64_t t = 5ull * rA;
+    while (t >= p) t -= p;
+    const uint32_t rB = (uint32_t)t;
+    const uint64_t base = ms - (uint64_t)m_lo;
+    const uint64_t xA = base + (rA >= rem ? rA - rem : rA + p - rem);
+    const uint64_t xB = base + (rB >= rem ? rB - rem : rB + p - rem);
+    if (xA < nbits) bA = (uint32_t)xA;
+    if (xB < nbits) bB = (uint32_t)xB;
+}
+
+// next hit of a progression: b + p (no 32-bit overflow: b < 2^30, and p >= 2^31
+// has a single hit in any mask)
+__device__ __forceinline__ uint32_t large_next(uint32_t b, uint32_t p, uint32_t nbits)
+{
+    return p >= 0x80000000u ? nbits : b + p;
+}
+
+__global__ void __launch_bounds__(kLargeBlock) large_mark_kernel(LargeArgs a)
 {
     const int64_t m_lo = a.g0 * 32;
     const int64_t m_hi = m_lo + 32 * (int64_t)a.nw;
     const uint32_t nbits = 32 * a.nw;
     const uint64_t n = a.i_end - a.i_begin;
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t pi = a.i_begin + (uint32_t)k;
-        const uint32_t p = __ldcs(a.primes + pi);
-        // the first multiple cleared is p^2 (= 6m + 1, class A): p itself stays set
-        const int64_t mmin = (int64_t)(((uint64_t)p * p - 1) / 6);
-        if (mmin >= m_hi) continue;
-        const uint64_t ms = (uint64_t)(mmin > m_lo ? mmin : m_lo);
-        const uint32_t rem = mod_magic(ms, p, __ldcs(a.magic + pi));
-        // m with p | 6m+1: m == -1/6 (mod p); p | 6m+5: m == -5/6 (mod p)
-        const uint64_t inv6 = (p % 6 == 1) ? (5ull * p + 1) / 6 : ((uint64_t)p + 1) / 6;
-        const uint32_t rA = p - (uint32_t)inv6;
-        uint64_t t = 5ull * rA;
-        while (t >= p) t -= p;
-        const uint32_t rB = (uint32_t)t;
-        const uint64_t base = ms - (uint64_t)m_lo;
-        uint64_t bA = base + (rA >= rem ? rA - rem : rA + p - rem);
-        uint64_t bB = base + (rB >= rem ? rB - rem : rB + p - rem);
-        for (; bA < nbits; bA += p) gmem_and(a.mask + (bA >> 5), clear_mask((uint32_t)bA));
-        for (; bB < nbits; bB += p) gmem_and(a.mask + a.stride + (bB >> 5), clear_mask((uint32_t)bB));
+    const uint64_t total = (uint64_t)gridDim.x * blockDim.x;
+    uint32_t *__restrict__ mA = a.mask;
+    uint32_t *__restrict__ mB = a.mask + a.stride;
+    const uint64_t pol = GB_LARGE_HINT ? l2_keep_policy() : 0;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += kLargeIlp * total) {
+        uint32_t bA[kLargeIlp], bB[kLargeIlp], pp[kLargeIlp];
+#pragma unroll
+        for (int j = 0; j < kLargeIlp; ++j) {
+            const uint64_t kk = k + j * total;
+            pp[j] = 1;
+            bA[j] = bB[j] = nbits;
+            if (kk < n) {
+                const uint32_t pi = a.i_begin + (uint32_t)kk;
+                pp[j] = __ldcs(a.primes + pi);
+                large_first_hits(pp[j], a.magic + pi, m_lo, m_hi, nbits, bA[j], bB[j]);
+            }
+        }
+        // all progressions of this thread advance together (one loop, predicated REDs)
+        bool more = true;
+        while (more) {
+            more = false;
+#pragma unroll
+            for (int j = 0; j < kLargeIlp; ++j) {
+                if (bA[j] < nbits) {
+                    gmem_and(mA + (bA[j] >> 5), clear_mask(bA[j]), pol);
+                    bA[j] = large_next(bA[j], pp[j], nbits);
+                }
+                if (bB[j] < nbits) {
+                    gmem_and(mB + (bB[j] >> 5), clear_mask(bB[j]), pol);
+                    bB[j] = large_next(bB[j], pp[j], nbits);
+                }
+                more |= (bA[j] < nbits) | (bB[j] < nbits);
+            }
+        }
     }
 }
 
@@ -390,8 +492,9 @@ cudaError_t launch_large(const LargeArgs &a, int num_sms, cudaStream_t st)
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || a.i_end <= a.i_begin) return e;
     const uint64_t n = a.i_end - a.i_begin;
-    const uint64_t nb = std::min<uint64_t>((n + 255) / 256, 64ull * num_sms);
-    large_mark_kernel<<<(unsigned)nb, 256, 0, st>>>(a);
+    if (a.nw >= (1u << 25)) return cudaErrorInvalidValue;      // 32-bit bit offsets (< 2^30)
+    const uint64_t nb = std::min<uint64_t>((n + kLargeBlock - 1) / kLargeBlock, (uint64_t)GB_LARGE_GRID_PER_SM * num_sms);
+    large_mark_kernel<<<(unsigned)nb, kLargeBlock, 0, st>>>(a);
     count_launch();
     return cudaGetLastError();
 }

@@ -222,8 +222,8 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
                     vb |= 0x1Fu;
                 }
                 if (lm) {   // K-LARGE mask of this chunk (primes above the carried range)
-                    va &= __ldcg(lm + (g - lg0));
-                    vb &= __ldcg(lm + lstride + (g - lg0));
+                    va &= __ldcs(lm + (g - lg0));          // read once: evict-first
+                    vb &= __ldcs(lm + lstride + (g - lg0));
                 }
             }
             wA[i] = va;

@@ -20,13 +20,13 @@ ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--time", type=int, default=0, help="time this many verify launches (after 2 warm-ups)")
 a = ap.parse_args()
 N = int(a.N)
-v = Verifier(hi_max=N + 1, p_max=a.p_max)
 lo = N + 1 - (1 << a.span)
+v = Verifier(hi_max=N + 1, p_max=a.p_max, origin=max(0, lo) & ~1)   # MAX_KEY: (n - origin)/2 < 2^40
 r = v.new_result()
 for _ in range(a.reps):
     v.verify(lo, N + 1, r)
 v.finalize(r)
-w = v.sieve_segment((lo - 3) // 128, (1 << a.span) // 128)
+w = v.sieve_segment((lo - 3) // 128, (1 << a.span) // 128 - 1)
 torch.cuda.synchronize()
 d = v.decode(r)
 print({k: d[k] for k in ("evens", "verified", "fastpath_unresolved", "max_pmin", "max_pmin_n", "chk")})
