@@ -310,7 +310,7 @@ def main():
         sieve = {"value": nbytes / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_launch": ms,
                  "odd_integers_per_s": 64 * (w_hi - w_lo) / (ms / 1e3),
                  "window": f"odd q in [{3 + 128 * w_lo}, {3 + 128 * w_hi})",
-                 "kernel": "segment_kernel (gb_sieve_segment)",
+                 "kernel": "sieve_out_kernel (gb_sieve_segment)",
                  "hbm_frac": nbytes / (ms / 1e3) / 1e9 / hbm, "hbm_peak_gbps": hbm}
         del out
 

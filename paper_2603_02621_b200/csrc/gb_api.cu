@@ -311,13 +311,69 @@ gb_status gb_sieve_segment(gb_ctx *ctx, uint64_t word_lo, uint64_t n_words, uint
     const uint64_t r = isqrt_u64(q_max);
     if (r > ctx->R) return GB_ERANGE;
     DeviceGuard g(ctx->device);
-    SegmentArgs sa;
-    sa.sp = sieve_primes(ctx, r);
-    sa.g_lo = 2 * word_lo;
-    sa.n_words32 = 2 * n_words;
-    sa.o_limit = UINT64_MAX;
-    sa.out = (uint32_t *)d_words;
-    return launch_segment(sa, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
+    cudaStream_t st = S(stream);
+    // output u32 words [w_lo, w_hi) <- class words [g_lo, g_hi), tiles of kTileWords
+    SieveOutArgs a;
+    a.sp = sieve_primes(ctx, r);
+    if (a.sp.i_big - a.sp.i_med > 1024) return GB_EINTERNAL;
+    a.w_lo = 2 * word_lo;
+    a.w_hi = 2 * (word_lo + n_words);
+    a.out = (uint32_t *)d_words;
+    const uint64_t g_lo = a.w_lo / 3, g_hi = (a.w_hi + 2) / 3;
+    a.tile_words = kTileWords;
+    const uint64_t n_tiles = (g_hi - g_lo + a.tile_words - 1) / a.tile_words;
+    a.carry = ctx->carry;
+    a.carry_stride = ctx->carry_stride;
+    a.n_carry = (uint32_t)std::min<uint64_t>(std::min<uint32_t>(a.sp.n_use, count_le(ctx->h_primes, kCarryPrimeMax)),
+                                             ctx->carry_stride);
+    a.med_idx = ctx->med_idx;
+    a.med_off = ctx->med_off;
+    a.i_b2 = count_le(ctx->h_primes, 16ull * (a.tile_words + 1));
+    a.i_b1 = count_le(ctx->h_primes, 32ull * (a.tile_words + 1));
+    a.lmask = nullptr;
+    a.lmask_g0 = 0;
+    a.lmask_stride = 0;
+    const size_t smem = 2 * 4ull * (a.tile_words + 1 + kWinSlackWords);
+    const int grid_max = (int)std::min<uint64_t>((uint64_t)ctx->num_sms, ctx->carry_ctas);
+    const uint32_t i_large = count_le(ctx->h_primes, kCarryPrimeMax);
+    const bool large = a.sp.n_use > i_large;
+    const uint32_t n_use_all = a.sp.n_use;
+    if (large) {
+        if (!ctx->lmask) return GB_EINTERNAL;
+        a.sp.n_use = i_large;
+    }
+    // chunks of whole tiles (one chunk unless K-LARGE masks are needed)
+    uint64_t chunk_tiles = n_tiles;
+    if (large) {
+        chunk_tiles = std::min<uint64_t>((ctx->lmask_stride - 64) / a.tile_words, (uint64_t)kLargeTilesPerSm * grid_max);
+        if (chunk_tiles > (uint64_t)grid_max) chunk_tiles -= chunk_tiles % (uint64_t)grid_max;
+        if (chunk_tiles == 0) return GB_EINTERNAL;
+    }
+    for (uint64_t t0 = 0; t0 < n_tiles; t0 += chunk_tiles) {
+        SieveOutArgs b = a;
+        const uint64_t nt = std::min<uint64_t>(chunk_tiles, n_tiles - t0);
+        b.g_first = g_lo + t0 * a.tile_words;
+        b.g_end = std::min<uint64_t>(g_hi, b.g_first + nt * a.tile_words);
+        b.n_tiles = nt;
+        if (large) {
+            LargeArgs L;
+            L.primes = ctx->primes;
+            L.magic = ctx->magic;
+            L.i_begin = i_large;
+            L.i_end = n_use_all;
+            L.g0 = (int64_t)b.g_first;
+            L.nw = (uint32_t)(b.g_end - b.g_first + 1);   // + the class-A word above the last tile
+            L.stride = ctx->lmask_stride;
+            L.mask = ctx->lmask;
+            b.lmask = ctx->lmask;
+            b.lmask_g0 = L.g0;
+            b.lmask_stride = L.stride;
+            if (launch_large(L, ctx->num_sms, st) != cudaSuccess) return GB_ECUDA;
+        }
+        const int grid = (int)std::min<uint64_t>((uint64_t)grid_max, nt);
+        if (launch_sieve_out(b, grid, smem, st) != cudaSuccess) return GB_ECUDA;
+    }
+    return GB_OK;
 }
 
 gb_status gb_result_init(int64_t *d_result, void *stream)

@@ -102,6 +102,28 @@ struct VerifyArgs {
     uint64_t lmask_stride;    // class B words start here
 };
 
+// gb_sieve_segment: the wheel-class window sieve of the verify kernel (shared memory,
+// carried offsets, K-LARGE mask) re-interleaved into the paper's odd layout.
+// Output u32 word W <-> odd q in [3 + 64W, 3 + 64W + 64); class word g <-> output
+// words 3g, 3g+1, 3g+2.
+struct SieveOutArgs {
+    SievePrimes sp;
+    uint64_t g_first, g_end;  // class words [g_first, g_end) (tiles of tile_words)
+    uint64_t n_tiles;
+    uint32_t tile_words;
+    uint64_t w_lo, w_hi;      // output u32 words [w_lo, w_hi) are written
+    uint32_t *out;            // out[W - w_lo]
+    uint32_t *carry;
+    uint64_t carry_stride;
+    uint32_t n_carry;
+    const uint16_t *med_idx;
+    const uint32_t *med_off;
+    uint32_t i_b2, i_b1;
+    const uint32_t *lmask;    // K-LARGE mask (nullable), word 0 <-> class word lmask_g0
+    int64_t lmask_g0;
+    uint64_t lmask_stride;
+};
+
 // Launchers (gb_kernels.cu).  Each returns the cudaGetLastError() of its launch.
 cudaError_t launch_seed(uint64_t s, uint32_t *primes, uint64_t *magic, uint4 *pk,
                         uint32_t *d_count, cudaStream_t st);
@@ -118,6 +140,7 @@ cudaError_t launch_large(const LargeArgs &a, int num_sms, cudaStream_t st);   //
 cudaError_t launch_is_prime(const uint64_t *x, uint8_t *out, uint64_t n, const uint64_t *bits,
                             uint64_t R, cudaStream_t st);
 cudaError_t configure_verify(size_t smem_max);
+cudaError_t launch_sieve_out(const SieveOutArgs &a, int grid, size_t smem, cudaStream_t st);
 int verify_blocks_per_sm(size_t smem);
 uint32_t unroll_p_max();       // largest prime of the unrolled class tables
 

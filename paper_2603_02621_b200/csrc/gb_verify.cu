@@ -784,6 +784,38 @@ __device__ __forceinline__ uint32_t take_special(uint32_t U, uint64_t u, uint32_
     return U;
 }
 
+// Steady primes of the window starting at class word g0 (thread 0): carried (the
+// previous tile was done by this CTA) and p^2 <= 6 m_lo + 1, i.e. the progression
+// started below the window.  ns_run: the running (monotone) count of this CTA.
+__device__ __forceinline__ uint32_t steady_count(const Carry6 &cy, int64_t g0, const SievePrimes &sp,
+                                                 uint32_t &ns_run)
+{
+    uint32_t ns = 0;
+    const int64_t m_lo = g0 * 32;
+    if (cy.have_prev && m_lo > 0) {
+        const uint64_t lim = 6 * (uint64_t)m_lo + 1;
+        const uint32_t top = min(cy.n_carry, sp.n_use);
+        ns = max(ns_run, sp.i_med);
+        if (ns == sp.i_med) {
+            uint32_t lo = sp.i_med, hi = top;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                const uint64_t pm = __ldg(sp.primes + mid);
+                if (pm * pm <= lim) lo = mid + 1; else hi = mid;
+            }
+            ns = lo;
+        } else {
+            while (ns < top) {
+                const uint64_t pm = __ldg(sp.primes + ns);
+                if (pm * pm > lim) break;
+                ++ns;
+            }
+        }
+        ns_run = ns;
+    }
+    return ns;
+}
+
 // dynamic shared memory: class A window | class B window | per-warp survivor queues
 extern __shared__ uint32_t g_win[];
 
@@ -956,32 +988,7 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(GB_PARAM)
         __syncthreads();                      // previous tile fully consumed
         if (tid == 0) {
             sh.next_round = 0;
-            // steady primes of this window: carried (previous tile done here) and
-            // p^2 <= 6 m_lo + 1, i.e. the progression started below the window
-            uint32_t ns = 0;
-            const int64_t m_lo = g0 * 32;
-            if (cy.have_prev && m_lo > 0) {
-                const uint64_t lim = 6 * (uint64_t)m_lo + 1;
-                const uint32_t top = min(cy.n_carry, a.sp.n_use);
-                ns = max(ns_run, a.sp.i_med);
-                if (ns == a.sp.i_med) {
-                    uint32_t lo = a.sp.i_med, hi = top;
-                    while (lo < hi) {
-                        const uint32_t mid = (lo + hi) >> 1;
-                        const uint64_t pm = __ldg(a.sp.primes + mid);
-                        if (pm * pm <= lim) lo = mid + 1; else hi = mid;
-                    }
-                    ns = lo;
-                } else {
-                    while (ns < top) {
-                        const uint64_t pm = __ldg(a.sp.primes + ns);
-                        if (pm * pm > lim) break;
-                        ++ns;
-                    }
-                }
-                ns_run = ns;
-            }
-            sh.ns = ns;
+            sh.ns = steady_count(cy, g0, a.sp, ns_run);
         }
         __syncthreads();
 #ifdef GB_PROFILE_PHASES
@@ -1089,6 +1096,72 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(GB_PARAM)
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// gb_sieve_segment: tiles of the wheel-class sieve (sieve6_window, as in the verify
+// kernel) written out in the paper's odd layout.  Odd q = 6m+1
+// (class A) is o = 3m - 1, q = 6m+3 is o = 3m (composite but for q = 3), q = 6m+5
+// (class B) is o = 3m + 1: the 96 odd bits [96g, 96g+96) hold B bits 32g..32g+31 at
+// o = 96g + 3j + 1 and A bits 32g+1..32g+32 at o = 96g + 3j + 2.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) sieve_out_kernel(const __grid_constant__ SieveOutArgs a)
+{
+    uint32_t *win = g_win;
+    const uint32_t nw_max = a.tile_words + 1 + kWinSlack;
+    uint32_t *wA = win, *wB = win + nw_max;
+    __shared__ uint32_t spread3[256];          // bit j of a byte -> bit 3j
+    __shared__ uint32_t sh_ns;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < 256; i += kThreads) {
+        uint32_t v = 0;
+        for (int j = 0; j < 8; ++j) v |= ((i >> j) & 1u) << (3 * j);
+        spread3[i] = v;
+    }
+    const uint64_t t_begin = (uint64_t)blockIdx.x * a.n_tiles / gridDim.x;
+    const uint64_t t_end = (uint64_t)(blockIdx.x + 1) * a.n_tiles / gridDim.x;
+    Carry6 cy;
+    cy.off = a.carry + (uint64_t)blockIdx.x * 2 * a.carry_stride;
+    cy.stride = a.carry_stride;
+    cy.n_carry = a.n_carry;
+    cy.have_prev = false;
+    cy.n_steady = 0;
+    cy.tile_m = 32 * a.tile_words;
+    uint32_t ns_run = 0;
+    for (uint64_t tile = t_begin; tile < t_end; ++tile) {
+        const uint64_t g0 = a.g_first + tile * a.tile_words;
+        const uint32_t tw = (uint32_t)min((uint64_t)a.tile_words, a.g_end - g0);
+        __syncthreads();                      // previous tile written out
+        if (tid == 0) sh_ns = steady_count(cy, (int64_t)g0, a.sp, ns_run);
+        __syncthreads();
+        cy.n_steady = sh_ns;
+        if (cy.tile_m == kTileM)
+            sieve6_window<true>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
+                                a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride);
+        else
+            sieve6_window<false>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
+                                 a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride);
+        cy.have_prev = true;
+        __syncthreads();
+        for (uint32_t i = tid; i < tw; i += kThreads) {
+            const uint32_t A = __funnelshift_r(wA[i], wA[i + 1], 1);   // A bits 32g+1 .. 32g+32
+            const uint32_t B = wB[i];
+            uint32_t v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                v[k] = (spread3[(A >> (8 * k)) & 0xFF] << 2) | (spread3[(B >> (8 * k)) & 0xFF] << 1);
+            const uint64_t g = g0 + i;
+            uint32_t o0 = v[0] | (v[1] << 24);
+            const uint32_t o1 = (v[1] >> 8) | (v[2] << 16);
+            const uint32_t o2 = (v[2] >> 16) | (v[3] << 8);
+            if (g == 0) o0 |= 1u;                                         // q = 3
+            const uint64_t W = 3 * g;
+            if (W >= a.w_lo && W < a.w_hi) a.out[W - a.w_lo] = o0;
+            if (W + 1 >= a.w_lo && W + 1 < a.w_hi) a.out[W + 1 - a.w_lo] = o1;
+            if (W + 2 >= a.w_lo && W + 2 < a.w_hi) a.out[W + 2 - a.w_lo] = o2;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
@@ -1104,6 +1177,20 @@ cudaError_t configure_verify(size_t smem_max)
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(verify_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     return e;
+}
+
+cudaError_t launch_sieve_out(const SieveOutArgs &a, int grid, size_t smem, cudaStream_t st)
+{
+    static size_t configured = 0;
+    if (smem > configured) {
+        const cudaError_t e = cudaFuncSetAttribute(sieve_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    sieve_out_kernel<<<grid, kThreads, smem, st>>>(a);
+    count_launch();
+    return cudaGetLastError();
 }
 
 int verify_blocks_per_sm(size_t smem)

@@ -62,6 +62,17 @@ def test_sieve_window_counts(V, a, b, count):
     assert n == count
 
 
+def test_sieve_segment_vs_oracle_4e18(V):
+    """K-SIEVE word for word against the oracle's byte sieve at the top of the C5
+    window (base primes up to 2e9: the K-LARGE mask path of gb_sieve_segment)."""
+    w_lo = (TOP - 3) // 128 - 4096
+    got = V.sieve_segment(w_lo, 4096).cpu().numpy().view(np.uint64)
+    a = 3 + 128 * w_lo
+    ob = oracle.sieve_window(a, a + 128 * 4096)
+    bits = np.packbits(ob, bitorder="little").view(np.uint64)
+    assert np.array_equal(got, bits)
+
+
 def test_golden_points(V):
     for n, p in read_pairs("pmin_points_4e18.txt"):
         got, d = V.run(n, n + 1, dump=True)

@@ -84,6 +84,8 @@ def test_kbase_resident_table(V):
     ((10**9 - 2**24 - 3) // 128, 2**24 // 128 + 5),
     ((10**12 - 2**24 - 3) // 128, 2**24 // 128),
     ((10**12 - 3) // 128 - 100000, 99999),
+    (1, 1), (2, 1), (30719, 3), (30720 * 3 - 7, 30720 + 11),     # one-word and tile-straddling windows
+    ((10**11) // 128 + 5, 3 * 30720 * 148 + 1001),              # more tiles than CTAs (carried offsets)
 ])
 def test_sieve_segment_parity(V, word_lo, n_words):
     got = V.sieve_segment(word_lo, n_words).cpu().numpy().view(np.uint64)
