@@ -184,6 +184,40 @@ __device__ __forceinline__ void mark_progression(uint32_t w, uint32_t off, uint3
     for (; i < n; ++i, ad += step) smem_and(ad, mask);
 }
 
+// Carried sieve offsets (per-CTA rows, ~92 MB at N = 1e12): L2 accesses with an
+// evict_last policy so the rows stay resident in L2 across tiles instead of making
+// a DRAM round trip per tile (GB_CARRY_NOHINT: plain .cg accesses, for A/B).
+__device__ __forceinline__ uint64_t carry_policy()
+{
+#ifdef GB_CARRY_NOHINT
+    return 0;
+#else
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+#endif
+}
+__device__ __forceinline__ uint32_t carry_ld(const uint32_t *p, uint64_t pol)
+{
+#ifdef GB_CARRY_NOHINT
+    (void)pol;
+    return __ldcg(p);
+#else
+    uint32_t v;
+    asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+#endif
+}
+__device__ __forceinline__ void carry_st(uint32_t *p, uint32_t v, uint64_t pol)
+{
+#ifdef GB_CARRY_NOHINT
+    (void)pol;
+    __stcg(p, v);
+#else
+    asm volatile("st.global.cg.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+#endif
+}
+
 template <bool DEF_TILE>
 __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
                               Carry6 *cy, const MedSched &ms, uint32_t i_b2, uint32_t i_b1,
@@ -308,6 +342,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
     const uint32_t s_end = ns > b_begin ? (ns < sp.n_use ? ns : sp.n_use) : b_begin;
     const uint32_t b2 = i_b2 < b_begin ? b_begin : (i_b2 < s_end ? i_b2 : s_end);
     const uint32_t b1 = i_b1 < b2 ? b2 : (i_b1 < s_end ? i_b1 : s_end);
+    const uint64_t cpol = carry_policy();
     uint32_t *__restrict__ cA = cy->off;                 // this CTA's carry row, class A
     uint32_t *__restrict__ cB = cy->off + cy->stride;    // class B
     const uint4 *__restrict__ pkp = sp.pk;
@@ -323,8 +358,8 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             if (pi < b2) {
                 const uint4 q = __ldg(pkp + pi);
                 pt[k] = make_uint2(q.x, tile_mod<DEF_TILE>(cy, q));
-                oa[k] = __ldcg(cA + pi);
-                ob[k] = __ldcg(cB + pi);
+                oa[k] = carry_ld(cA + pi, cpol);
+                ob[k] = carry_ld(cB + pi, cpol);
             } else {
                 pt[k] = make_uint2(1, 0);
                 oa[k] = ob[k] = nbits;
@@ -337,8 +372,8 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             for (uint32_t b = ob[k]; b < nbits; b += p) clear_bit(sB, b);
             const uint32_t pi = p0 + k * nt;
             if (pi < b2) {
-                __stcg(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm);
-                __stcg(cB + pi, ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm);
+                carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
+                carry_st(cB + pi, ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm, cpol);
             }
         }
         __syncwarp();   // reconverge: the per-lane hit loops diverge
@@ -355,8 +390,8 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
                 const uint4 q = __ldg(pkp + pi);
                 pp[k] = q.x;
                 tt[k] = tile_mod<DEF_TILE>(cy, q);
-                oa[k] = __ldcg(cA + pi);
-                ob[k] = __ldcg(cB + pi);
+                oa[k] = carry_ld(cA + pi, cpol);
+                ob[k] = carry_ld(cB + pi, cpol);
             } else {
                 pp[k] = nbits; tt[k] = 0;
                 oa[k] = ob[k] = nbits;
@@ -371,8 +406,8 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             if (ob[k] + p < nbits) clear_bit(sB, ob[k] + p);
             const uint32_t pi = p0 + k * nt;
             if (pi < b1) {
-                __stcg(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm);
-                __stcg(cB + pi, ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm);
+                carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
+                carry_st(cB + pi, ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm, cpol);
             }
         }
     }
@@ -387,8 +422,8 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
                 const uint4 q = __ldg(pkp + pi);
                 pp[k] = q.x;
                 tt[k] = tile_mod<DEF_TILE>(cy, q);
-                oa[k] = __ldcg(cA + pi);
-                ob[k] = __ldcg(cB + pi);
+                oa[k] = carry_ld(cA + pi, cpol);
+                ob[k] = carry_ld(cB + pi, cpol);
             } else {
                 pp[k] = nbits; tt[k] = 0;
                 oa[k] = ob[k] = nbits;
@@ -401,8 +436,8 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             if (ob[k] < nbits) clear_bit(sB, ob[k]);
             const uint32_t pi = p0 + k * nt;
             if (pi < s_end) {
-                __stcg(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm);
-                __stcg(cB + pi, ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm);
+                carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
+                carry_st(cB + pi, ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm, cpol);
             }
         }
     }
