@@ -42,6 +42,9 @@ def parse():
                     help="c4: every even n in [4, N] (the metric's workload); c5: the window "
                          "[4e18 - 1e11, 4e18) of BASELINE.json configs[4]")
     ap.add_argument("--p-max", type=int, default=65521)
+    ap.add_argument("--mode", default="bulk", choices=["bulk", "pern"],
+                    help="bulk: the product path (inverted bulk marking); pern: the paper's per-n "
+                         "gpu3 kernel (NEXT-1 comparison, PAPER.md:82-95)")
     ap.add_argument("--strips-per-rank", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -184,7 +187,7 @@ def main():
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-            V.verify(a, b, r, p_max=args.p_max)
+            V.verify(a, b, r, p_max=args.p_max, mode=args.mode)
             if k_events is not None:
                 e1.record(stream)
                 k_events.append((e0, e1))
@@ -325,7 +328,8 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "u64",
                 "data": "synthetic (deterministic number-theoretic range; no dataset)",
                 "config": {"workload": desc, "lo": lo, "hi": hi, "p_max": args.p_max, "strips_per_rank": args.strips_per_rank,
-                           "parallelism": f"range-sharded x{world}", "l2": "flushed between steps"},
+                           "parallelism": f"range-sharded x{world}", "l2": "flushed between steps",
+                           "mode": args.mode},
                 "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "roofline": roofline,
                 "cpu_baseline": cpu, "sieve": sieve,
                 "result": {k: res[k] for k in ("evens", "verified", "fastpath_unresolved", "unresolved",

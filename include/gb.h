@@ -110,7 +110,11 @@ gb_status gb_ctx_tables(const gb_ctx *ctx, const uint64_t **d_bits, const uint32
  * Eratosthenes to determine the primality of all odd integers in that
  * segment"): writes n_words 64-bit words of the global odd bitset,
  *   bit b of d_words[i]  <->  odd q = 3 + 2*(64*(word_lo + i) + b), 1 = prime.
- * Needs isqrt(largest q) <= R, else GB_ERANGE.  d_words 8-byte aligned. */
+ * Needs isqrt(largest q) <= R, else GB_ERANGE.  d_words 8-byte aligned.
+ * Implementation: the verify kernel's shared-memory wheel sieve (persistent CTAs
+ * with carried offsets, K-LARGE mask for primes > 2^21) re-interleaved into this
+ * layout.  Uses the ctx's carry rows: do not overlap with another call on the
+ * same ctx. */
 gb_status gb_sieve_segment(gb_ctx *ctx, uint64_t word_lo, uint64_t n_words,
                            uint64_t *d_words, void *stream);
 
@@ -131,7 +135,10 @@ gb_status gb_result_finalize(int64_t *d_result, void *stream);
  * ACCUMULATES into d_result (initialised once by gb_result_init), so disjoint
  * calls compose.  d_pmin_dump (nullable): one u32 per even n in [lo_e, hi),
  * lo_e = max(4, lo rounded up to even), index (n - lo_e)/2, value p_min, 0 =
- * unresolved.  Launches exactly one kernel (zero for an empty range).
+ * unresolved.  Launches one kernel (zero for an empty range); when the range
+ * needs sieving primes above 2^21 (hi > 4.4e12, e.g. the 4e18 window) it runs in
+ * chunks of whole tiles, each a K-LARGE mask fill + marking launch and a verify
+ * launch.
  * Errors: GB_EINVAL (p_max < 3 or > the ctx's p_max, hi > GB_HI_LIMIT,
  * n < origin, (hi - origin)/2 >= 2^40, misaligned pointers), GB_ERANGE
  * (hi > ctx hi_max). */
@@ -151,6 +158,19 @@ gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_m
  * chunks).  Synchronizes `stream`. */
 gb_status gb_verify_range_host(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_max,
                                int64_t *h_result, uint32_t *h_pmin_dump, void *stream);
+
+/* NEXT-1 comparison mode: the paper's own gpu3 Phase-1
+ * kernel (section 2.3.2, Fig. 1) -- one thread per even n scans
+ * odd primes p <= p_max ascending and tests q = n - p by the three-way oracle:
+ * q <= R -> the resident small-prime bitset; q in the current
+ * segment -> that segment's odd bitset, sieved by gb_sieve_segment into ctx
+ * scratch (segments of 2^28 evens); otherwise deterministic MR64
+ * (PAPER.md:89).  Unresolved n go to the same exhaustive fallback.  Same
+ * arguments, result semantics and errors as gb_verify_range, and results identical
+ * to it field by field; two launches per segment.  Not the product path: it
+ * exists to measure per-n lookups against the inverted bulk marking on one box. */
+gb_status gb_verify_range_pern(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_max,
+                               int64_t *d_result, uint32_t *d_pmin_dump, void *stream);
 
 /* Deterministic 64-bit Miller-Rabin (12 prime bases 2..37; PAPER.md:89,
  * SPEC.md:128) as used by the fallback: d_out[i] = 1 iff d_x[i] is prime. */

@@ -33,7 +33,7 @@ constexpr uint64_t kMaxSms = 160;   // workspace sizing bound (B200: 148)
 struct Layout {
     uint64_t R, bits_words, list_cap, n_blk, carry_stride, carry_ctas, lmask_stride;
     uint64_t off_bits, off_primes, off_magic, off_tmod, off_carry, off_lmask, off_sched, off_blk, off_counter,
-        off_res, off_dump, total;
+        off_res, off_dump, off_seg, total;
 };
 
 // pi(x) upper bound (Rosser-Schoenfeld: pi(x) < 1.25506 x / ln x for x > 1) + slack
@@ -78,6 +78,7 @@ bool plan(uint64_t hi_max, uint32_t p_max, Layout &L)
     L.off_counter = o; o = align_up(o + 256, 256);
     L.off_res = o;     o = align_up(o + 8 * (uint64_t)GB_RESULT_WORDS, 256);
     L.off_dump = o;    o = align_up(o + 4 * kDumpScratch, 256);
+    L.off_seg = o;     o = align_up(o + 8 * (kPerNSegEvens / 64 + 4), 256);
     L.total = o;
     return true;
 }
@@ -191,6 +192,7 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
     c->counter = (uint32_t *)(ws + L.off_counter);
     c->res_scratch = (int64_t *)(ws + L.off_res);
     c->dump_scratch = (uint32_t *)(ws + L.off_dump);
+    c->seg_scratch = (uint64_t *)(ws + L.off_seg);
     if (cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
         delete c;
         return GB_ECUDA;
@@ -522,6 +524,55 @@ gb_status gb_verify_range_host(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p
                         st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
         return GB_ECUDA;
+    return GB_OK;
+}
+
+gb_status gb_verify_range_pern(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_max, int64_t *d_result,
+                               uint32_t *d_pmin_dump, void *stream)
+{
+    if (!ctx || !d_result || ((uintptr_t)d_result & 7) || ((uintptr_t)d_pmin_dump & 3)) return GB_EINVAL;
+    if (lo > hi || hi > GB_HI_LIMIT || p_max < 3 || p_max > ctx->p_max) return GB_EINVAL;
+    const uint64_t lo_e = lo < 4 ? 4 : lo + (lo & 1);
+    if (hi <= lo_e) return GB_OK;
+    if (hi > ctx->hi_max) return GB_ERANGE;
+    if (lo_e < ctx->origin || ((hi - ctx->origin) >> 1) >= (1ull << GB_KEY_SHIFT)) return GB_EINVAL;
+    const uint32_t n_cand = count_le(ctx->h_primes, p_max);
+    if (n_cand == 0) return GB_EINVAL;
+    DeviceGuard g(ctx->device);
+    // words of the global odd bitset the ctx can sieve: isqrt(q) <= R for every q
+    const uint64_t q_cap = (ctx->R + 1) * (ctx->R + 1) - 1;          // largest q with isqrt(q) <= R
+    const uint64_t w_cap = q_cap >= 130 ? (q_cap - 130) / 128 : 0;   // words [0, w_cap] fit
+    for (uint64_t s0 = lo_e; s0 < hi; s0 += 2 * kPerNSegEvens) {
+        const uint64_t s1 = std::min<uint64_t>(hi, s0 + 2 * kPerNSegEvens);
+        PerNArgs a;
+        a.n_first = s0;
+        a.n_evens = (s1 - s0 + 1) / 2;
+        // segment bitset: odd q in [s0, s1), word aligned
+        const uint64_t qa = s0 > 3 ? s0 - 1 : 3;
+        uint64_t w0 = (qa - 3) / 128, w1 = (s1 - 1 - 3) / 128 + 1;
+        w1 = std::min<uint64_t>(w1, w_cap + 1);
+        if (w1 <= w0) w1 = w0;
+        a.seg_bits = ctx->seg_scratch;
+        a.seg_word_lo = w0;
+        a.seg_q_lo = 3 + 128 * w0;
+        a.seg_q_hi = 3 + 128 * w1;
+        if (w1 > w0) {
+            const gb_status st = gb_sieve_segment(ctx, w0, w1 - w0, ctx->seg_scratch, stream);
+            if (st != GB_OK) return st;
+        }
+        a.n_cand = n_cand;
+        a.primes = ctx->primes;
+        a.n_base = (uint32_t)ctx->n_base;
+        a.base_bits = ctx->bits;
+        a.R = ctx->R;
+        a.p_fallback = (uint64_t)ctx->h_primes[n_cand - 1] + 2;
+        a.cap = UINT64_MAX;
+        a.origin = ctx->origin;
+        a.lo_e = lo_e;
+        a.result = d_result;
+        a.dump = d_pmin_dump;
+        if (launch_pern(a, S(stream)) != cudaSuccess) return GB_ECUDA;
+    }
     return GB_OK;
 }
 

@@ -124,6 +124,25 @@ struct SieveOutArgs {
     uint64_t lmask_stride;
 };
 
+// NEXT-1 (gb_pern.cu): the paper's per-n gpu3 Phase-1 kernel over one segment.
+constexpr uint64_t kPerNSegEvens = 1ull << 28;   // evens per segment (paper: SEG_SIZE = 1e7; larger here so
+                                                 // gb_sieve_segment fills the GPU, bitset 32 MB in L2)
+struct PerNArgs {
+    uint64_t n_first, n_evens;     // evens n_first, n_first + 2, ...
+    uint32_t n_cand;               // odd primes p <= p_max
+    const uint32_t *primes;
+    uint32_t n_base;
+    const uint64_t *base_bits;     // resident odd bitset of [3, R]
+    uint64_t R;
+    const uint64_t *seg_bits;      // segment odd bitset, word 0 <-> global word seg_word_lo
+    uint64_t seg_word_lo;
+    uint64_t seg_q_lo, seg_q_hi;   // odd q in [seg_q_lo, seg_q_hi) are in seg_bits
+    uint64_t p_fallback, cap, origin, lo_e;
+    int64_t *result;
+    uint32_t *dump;
+};
+cudaError_t launch_pern(const PerNArgs &a, cudaStream_t st);
+
 // Launchers (gb_kernels.cu).  Each returns the cudaGetLastError() of its launch.
 cudaError_t launch_seed(uint64_t s, uint32_t *primes, uint64_t *magic, uint4 *pk,
                         uint32_t *d_count, cudaStream_t st);
@@ -171,6 +190,7 @@ struct gb_ctx {
     uint32_t *counter;     // K-BASE scratch
     int64_t *res_scratch;  // host API result
     uint32_t *dump_scratch;
+    uint64_t *seg_scratch;  // NEXT-1 per-n mode: one segment's odd bitset
     uint64_t n_base;
     std::vector<uint32_t> h_primes;  // host copy for range planning
 };

@@ -63,6 +63,7 @@ _sigs = {
     "gb_verify_range": (ctypes.c_int, [_vp, _u64, _u64, _u32, _vp, _vp, _vp]),
     "gb_verify_range_ex": (ctypes.c_int, [_vp, _u64, _u64, _u32, _u64, _vp, _vp, _vp]),
     "gb_verify_range_host": (ctypes.c_int, [_vp, _u64, _u64, _u32, _vp, _vp, _vp]),
+    "gb_verify_range_pern": (ctypes.c_int, [_vp, _u64, _u64, _u32, _vp, _vp, _vp]),
     "gb_is_prime_u64": (ctypes.c_int, [_vp, _vp, _u64, _vp]),
     "gb_launch_count": (_u64, []),
     "gb_status_string": (ctypes.c_char_p, [ctypes.c_int]),
@@ -135,6 +136,11 @@ def gb_result_finalize(d_result, stream) -> None:
 def gb_verify_range(ctx: int, lo: int, hi: int, p_max: int, d_result, d_dump, stream) -> None:
     _check(_lib.gb_verify_range(ctx, lo, hi, p_max, _ptr(d_result), _ptr(d_dump),
                                 _ptr_stream(stream)), "gb_verify_range")
+
+
+def gb_verify_range_pern(ctx: int, lo: int, hi: int, p_max: int, d_result, d_dump, stream) -> None:
+    _check(_lib.gb_verify_range_pern(ctx, lo, hi, p_max, _ptr(d_result), _ptr(d_dump), _ptr_stream(stream)),
+           "gb_verify_range_pern")
 
 
 def gb_verify_range_ex(ctx: int, lo: int, hi: int, p_max: int, cap: int, d_result, d_dump,

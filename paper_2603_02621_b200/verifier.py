@@ -42,22 +42,28 @@ class Verifier:
 
     # -- operations --------------------------------------------------------------
     def verify(self, lo: int, hi: int, result: torch.Tensor, p_max: int | None = None,
-               dump: torch.Tensor | None = None, cap: int | None = None) -> None:
+               dump: torch.Tensor | None = None, cap: int | None = None, mode: str = "bulk") -> None:
+        """mode "bulk": the product path (inverted bulk marking); "pern": the paper's
+        per-n gpu3 kernel (NEXT-1 comparison mode)."""
         p = self.p_max if p_max is None else p_max
-        if cap is None:
+        if mode == "pern":
+            if cap is not None:
+                raise ValueError("the per-n mode has no fallback cap hook")
+            gb.gb_verify_range_pern(self.ctx, lo, hi, p, result, dump, self.stream)
+        elif cap is None:
             gb.gb_verify_range(self.ctx, lo, hi, p, result, dump, self.stream)
         else:
             gb.gb_verify_range_ex(self.ctx, lo, hi, p, cap, result, dump, self.stream)
 
     def run(self, lo: int, hi: int, p_max: int | None = None, dump: bool = False,
-            cap: int | None = None):
+            cap: int | None = None, mode: str = "bulk"):
         """init + verify + finalize; returns (decoded dict, dump tensor or None)."""
         r = self.new_result()
         d = None
         if dump:
             e = 4 if lo < 4 else lo + (lo & 1)
             d = torch.zeros(max(0, (hi - e + 1) // 2), dtype=torch.int32, device=self.device)
-        self.verify(lo, hi, r, p_max=p_max, dump=d if (d is not None and d.numel()) else None, cap=cap)
+        self.verify(lo, hi, r, p_max=p_max, dump=d if (d is not None and d.numel()) else None, cap=cap, mode=mode)
         self.finalize(r)
         self.stream.synchronize()
         return self.decode(r), d

@@ -8,6 +8,7 @@ is appended to a resumable JSONL cache.  Nothing here touches the CUDA path:
 every stored value comes from oracle/ (see the oracle's header for citations).
 
 usage: python scripts/make_golden.py --N 1e12 [--threads 6] [--piece 1e10]
+       python scripts/make_golden.py --window c5 --piece 1e10   (the 4e18 window)
 """
 import argparse
 import json
@@ -47,14 +48,19 @@ def to_json_result(r):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--N", type=float, required=True)
+    ap.add_argument("--N", type=float, default=None, help="the range [4, N]")
+    ap.add_argument("--window", choices=["c5"], default=None,
+                    help="c5: [4e18 - 1e11, 4e18) (BASELINE.json configs[4])")
     ap.add_argument("--threads", type=int, default=oracle.default_threads())
     ap.add_argument("--piece", type=float, default=1e10)
     ap.add_argument("--p-fast", type=int, default=65521)
     args = ap.parse_args()
-    N = int(args.N)
     piece = int(args.piece)
-    tag = f"{N:.0e}".replace("+", "")
+    if args.window == "c5":
+        LO, HI, tag = 4 * 10**18 - 10**11, 4 * 10**18, "c5_4e18"
+    else:
+        N = int(args.N)
+        LO, HI, tag = 4, N + 1, f"{N:.0e}".replace("+", "")
     cache = os.path.join(ROOT, "tests", "golden", f".cache_verify_{tag}.jsonl")
     outp = os.path.join(ROOT, "tests", "golden", f"verify_{tag}.json")
     done = {}
@@ -65,9 +71,9 @@ def main():
                 done[(rec["lo"], rec["hi"])] = rec
     total = None
     t_all = 0.0
-    lo = 4
-    while lo < N + 1:
-        hi = min(lo + piece, N + 1)
+    lo = LO
+    while lo < HI:
+        hi = min(lo + piece, HI)
         if (lo, hi) not in done:
             t0 = time.time()
             r, _ = oracle.verify(lo, hi, p_fast=args.p_fast, threads=args.threads)
@@ -85,7 +91,7 @@ def main():
         total = merge(total, res)
         lo = hi
     total["hist"] = {str(k): v for k, v in sorted(total["hist"].items())}
-    doc = {"lo": 4, "hi": N + 1, "p_fast": args.p_fast,
+    doc = {"lo": LO, "hi": HI, "p_fast": args.p_fast,
            "chk_def": "sum p_min(n)*floor(n/192) mod 2^64 (DESIGN.md R6)",
            "source": "oracle/gb_oracle.c via scripts/make_golden.py (CPU oracle only)",
            "oracle_seconds": round(t_all, 1), "result": total}

@@ -103,6 +103,16 @@ def test_windows_vs_oracle_golden(V):
         assert hashlib.sha256(dd.tobytes()).hexdigest() == w["dump_sha256"], w["lo"]
 
 
+def test_pern_mode_golden_window(V):
+    """NEXT-1 per-n kernel (three-way oracle: small bitset / segment bitset / MR64)
+    on the top golden window: same aggregates and per-n dump hash."""
+    w = _golden()["windows"][0]
+    got, d = V.run(w["lo"], w["hi"], dump=True, mode="pern")
+    for k in oracle.FIELDS:
+        assert got[k] == w["result"][k], k
+    assert hashlib.sha256(d.cpu().numpy().astype("<u4").tobytes()).hexdigest() == w["dump_sha256"]
+
+
 def test_chunk_boundaries_and_composition(V):
     """A range spanning several K-LARGE chunks equals the sum of pieces whose chunk
     boundaries fall elsewhere, aggregate by aggregate and n by n (P13)."""
