@@ -244,12 +244,7 @@ def test_golden_files_match_appendix(N, tag):
 
 def test_golden_1e12_closed_forms():
     """1e12 golden (oracle only) vs published pi(1e12), pi2(1e12)."""
-    path = os.path.join(GOLDEN, "verify_1e12.json")
-    if not os.path.exists(path):
-        path = os.path.join(GOLDEN, "verify_1e12_chk64.json")
-    if not os.path.exists(path):
-        pytest.skip("golden not generated")
-    g = json.load(open(path))["result"]
+    g = json.load(open(os.path.join(GOLDEN, "verify_1e12.json")))["result"]
     assert g["evens"] == 10**12 // 2 - 1
     assert g["hist"]["2"] == PUB["pi"]["1000000000000"] - 1 == 37607912017
     assert g["hist"]["3"] == PUB["pi"]["1000000000000"] - 1 - PUB["pi2"]["1000000000000"] == 35737326797
