@@ -161,9 +161,16 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # one process per GPU; GB_DIST_BACKEND=gloo lets a multi-rank run share one GPU
+    # (a functional check of the N > 1 path on a 1-GPU box; NCCL refuses that)
+    backend = os.environ.get("GB_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import __graft_entry__
     __graft_entry__.build() if rank == 0 else None
     if world > 1:
