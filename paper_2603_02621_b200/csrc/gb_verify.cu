@@ -346,7 +346,10 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
     uint32_t *__restrict__ cA = cy->off;                 // this CTA's carry row, class A
     uint32_t *__restrict__ cB = cy->off + cy->stride;    // class B
     const uint4 *__restrict__ pkp = sp.pk;
-    constexpr int kB = 4;
+#ifndef GB_KB
+#define GB_KB 2
+#endif
+    constexpr int kB = GB_KB;
     // steady primes with p <= full window / 2: hit loops (>= 2 hits per class)
     for (uint32_t w0 = b_begin + (tid & ~31u); w0 < b2; w0 += kB * nt) {   // warp-uniform trips
         const uint32_t p0 = w0 + lane;
@@ -379,7 +382,10 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
         __syncwarp();   // reconverge: the per-lane hit loops diverge
     }
     // steady primes with window/2 < p <= window: at most 2 hits per class, predicated
-    constexpr int kB2 = 8;
+#ifndef GB_KB2
+#define GB_KB2 2
+#endif
+    constexpr int kB2 = GB_KB2;
     for (uint32_t w0 = b2 + (tid & ~31u); w0 < b1; w0 += kB2 * nt) {
         const uint32_t p0 = w0 + lane;
         uint32_t pp[kB2], tt[kB2], oa[kB2], ob[kB2];
