@@ -133,3 +133,21 @@ def test_chunk_boundaries_and_composition(V):
     assert got["hist"] == whole["hist"]
     assert torch.equal(torch.cat(parts), dw)
     assert whole["verified"] == whole["evens"] == span // 2 and whole["unresolved"] == 0
+
+
+def test_full_c5_window_vs_oracle_golden(V):
+    """Config C5 in full: every even n in [4e18 - 1e11, 4e18) (5e10 evens), all
+    aggregates and the histogram vs the oracle's golden (scripts/make_golden.py
+    --window c5; 1,572 s on 8 host cores)."""
+    import json as _json
+    path = os.path.join(GOLDEN, "verify_c5_4e18.json")
+    doc = _json.load(open(path))
+    assert doc["chk_def"].startswith(CHK_DEF)
+    got, _ = V.run(BOT, TOP)
+    g = doc["result"]
+    for k in oracle.FIELDS:
+        assert got[k] == g[k], (k, got[k], g[k])
+    hist = np.zeros(oracle.NBINS, np.int64)
+    for i, c in g["hist"].items():
+        hist[int(i)] = c
+    assert np.array_equal(np.asarray(got["hist"]), hist)

@@ -266,3 +266,15 @@ def test_golden_4e18_windows_match_appendix():
     for r in w.values():
         assert r["evens"] == r["verified"] and r["fastpath_unresolved"] == 0 and r["unresolved"] == 0
         assert sum(r["hist"].values()) == r["evens"]
+
+
+def test_golden_c5_window_consistency():
+    """The full C5 golden (oracle only): 5e10 evens, all verified on the fast path,
+    histogram sums to the evens, p_min below the known bound 9,781 for n <= 4e18
+    (SURVEY P9), and its maximum is at least the top window's 3,191 (Appendix A)."""
+    g = json.load(open(os.path.join(GOLDEN, "verify_c5_4e18.json")))["result"]
+    assert g["evens"] == g["verified"] == 5 * 10**10
+    assert g["fastpath_unresolved"] == 0 and g["unresolved"] == 0
+    assert sum(g["hist"].values()) == g["evens"]
+    assert 3191 <= g["max_pmin"] <= 9781
+    assert 4 * 10**18 - 10**11 <= g["max_pmin_n"] < 4 * 10**18
