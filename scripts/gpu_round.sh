@@ -40,6 +40,12 @@ for w in $what; do
         --log-file gpurun_out/launches_c5.csv python bench.py --workload c5 --steps 1 --warmup 1 --no-cpu-baseline \
         > gpurun_out/bench_c5_under_ncu.log 2>&1
       echo "ncu c5 launches rc=$?" ;;
+    sanitize)
+      for tool in memcheck racecheck synccheck initcheck; do
+        timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_driver.py \
+          > gpurun_out/sanitize_$tool.log 2>&1
+        echo "sanitize $tool rc=$?"; tail -2 gpurun_out/sanitize_$tool.log
+      done ;;
     time)
       timeout 600 python scripts/prof_one.py --span 36 --time 10 2>&1 | tail -2 ;;
   esac
