@@ -99,14 +99,14 @@ constexpr uint32_t kVerifyDynSmemMax = 168 * 1024;   // the two windows; + queue
 constexpr uint32_t kWinSlackWords = 128;   // = kWinSlack in gb_verify.cu
 uint32_t verify_tile_words(uint32_t halo)
 {
-    if (2 * 4ull * (halo + kTileWords + kWinSlackWords) <= kVerifyDynSmemMax) return kTileWords;
-    const uint32_t tw = (kVerifyDynSmemMax / 8 - halo - kWinSlackWords) & ~127u;   // multiple of 128 words
+    if (kSlots * 2 * 4ull * (halo + kTileWords + kWinSlackWords) <= kVerifyDynSmemMax) return kTileWords;
+    const uint32_t tw = (kVerifyDynSmemMax / (8 * kSlots) - halo - kWinSlackWords) & ~127u;   // multiple of 128 words
     return tw;
 }
-constexpr size_t kQueueBytes = (kThreads / 32) * 128 * 6;   // per-warp survivor queues (u32 U + u16 index)
+constexpr size_t kQueueBytes = kMarkWarps * 128 * 6;   // per-warp survivor queues (u32 U + u16 index)
 size_t verify_smem(uint32_t halo)
 {
-    return 2 * 4ull * (halo + verify_tile_words(halo) + kWinSlackWords) + kQueueBytes;
+    return kSlots * 2 * 4ull * (halo + verify_tile_words(halo) + kWinSlackWords) + kQueueBytes;
 }
 
 SievePrimes sieve_primes(const gb_ctx *c, uint64_t sqrt_bound)
@@ -248,7 +248,7 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
         const uint32_t i_med = count_le(c->h_primes, 31), i_big = count_le(c->h_primes, kWarpPrimeMax);
         const uint32_t nmed = i_big > i_med ? i_big - i_med : 0;
         if (nmed > 1024) { delete c; return GB_EINTERNAL; }
-        const int nw = kThreads / 32;
+        const int nw = kSieveWarps;                    // warps that sieve (gb_verify.cu)
         const uint32_t h0 = verify_halo(c->h_primes[count_le(c->h_primes, p_max) - 1]);
         const double nbits = 32.0 * (h0 + verify_tile_words(h0));
         std::vector<std::vector<uint16_t>> lists(nw);

@@ -15,10 +15,29 @@ namespace gb {
 #define GB_THREADS 1024
 #endif
 constexpr int kThreads = GB_THREADS;       // threads per CTA, every kernel
+// Warp specialization of the verify kernel (GB_WS=1, an A/B option): kSieveWarps
+// warps sieve tile t+1 into one window slot while the other warps mark tile t from
+// the other slot (two half-size slots).  Measured slower than the default: at best
+// 42.8 ms (16 sieving warps) vs 38.3 ms on the 2^36 profile span -- the sieve is
+// latency bound and scales with its warp count, and half tiles double the
+// per-prime work per even.
+#ifndef GB_WS
+#define GB_WS 0
+#endif
+#ifndef GB_SIEVE_WARPS
+#define GB_SIEVE_WARPS 12
+#endif
 #ifndef GB_TILE_WORDS
+#if GB_WS
+#define GB_TILE_WORDS 10240
+#else
 #define GB_TILE_WORDS 20480
 #endif
+#endif
 constexpr int kTileWords = GB_TILE_WORDS;  // verify tile: 32-bit words per mod-6 class
+constexpr int kSlots = GB_WS ? 2 : 1;      // window slots of the verify kernel
+constexpr int kSieveWarps = GB_WS ? GB_SIEVE_WARPS : GB_THREADS / 32;   // warps that sieve (medium LPT schedule)
+constexpr int kMarkWarps = GB_WS ? GB_THREADS / 32 - GB_SIEVE_WARPS : GB_THREADS / 32;   // warps that mark
 constexpr uint32_t kTileM = 32u * kTileWords;  // m-span of a tile (n = 6m + a): 786432 evens
 constexpr int kSieveTileWords = 16384;     // 32-bit words per gb_sieve_segment CTA
 constexpr int kHistSmem = 1024;            // histogram bins kept in shared memory
@@ -32,7 +51,7 @@ constexpr int kScanBlockWords = 2048;      // u64 words per K-BASE compaction bl
 constexpr uint32_t kCarryPrimeMax = 1u << 21;  // verify CTAs carry sieve offsets of primes below
 constexpr int kMaxBlocksPerSm = 4;         // sizing bound for per-CTA carry storage
 #ifndef GB_LARGE_TILES_PER_SM
-#define GB_LARGE_TILES_PER_SM 3
+#define GB_LARGE_TILES_PER_SM (GB_WS ? 6 : 3)
 #endif
 // Ranges that need sieving primes above kCarryPrimeMax (hi > 2^42, e.g. the 4e18
 // window) run in chunks of GB_LARGE_TILES_PER_SM verify tiles per SM; before each

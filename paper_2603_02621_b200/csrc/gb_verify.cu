@@ -27,9 +27,6 @@
 
 namespace gb {
 
-#ifdef GB_PROFILE_PHASES
-__device__ unsigned long long g_prof[5];
-#endif
 
 // ---------------------------------------------------------------------------
 // transitions and compile-time class tables
@@ -218,14 +215,25 @@ __device__ __forceinline__ void carry_st(uint32_t *p, uint32_t v, uint64_t pol)
 #endif
 }
 
-template <bool DEF_TILE>
+// barrier of the NT threads that run sieve6_window: the whole CTA, or (warp-
+// specialized verify kernel) the sieving warps 0 .. NT/32-1 on named barrier 1
+template <int NT>
+__device__ __forceinline__ void group_sync()
+{
+    if constexpr (NT == kThreads) __syncthreads();
+    else asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
+// K-SIEVE of one tile's two class windows by NT threads (gtid = 0 .. NT-1, whole
+// warps); ends WITHOUT a barrier
+template <bool DEF_TILE, int NT>
 __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
                               Carry6 *cy, const MedSched &ms, uint32_t i_b2, uint32_t i_b1,
-                              const uint32_t *__restrict__ lm, int64_t lg0, uint64_t lstride)
+                              const uint32_t *__restrict__ lm, int64_t lg0, uint64_t lstride, int gtid)
 {
-    const int tid = threadIdx.x;
+    const int tid = gtid;
     const uint32_t lane = (uint32_t)tid & 31;
-    constexpr int nt = kThreads;
+    constexpr int nt = NT;
     const uint32_t sA = smem_addr(wA), sB = smem_addr(wB);
     // Phase T: primes 5..31 by shifted word patterns, per-thread incremental phases
     {
@@ -322,10 +330,10 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
         sh_hA[pi - sp.i_med] = (uint16_t)(oa < nbits ? (nbits - oa + k.x - 1) / k.x : 0);
         sh_hB[pi - sp.i_med] = (uint16_t)(ob < nbits ? (nbits - ob + k.x - 1) / k.x : 0);
     }
-    __syncthreads();
+    group_sync<NT>();
     // one warp per medium prime: the host's LPT schedule (longest work first onto
-    // the least-loaded warp) gives every warp the same share, with no atomics
-    {
+    // the least-loaded warp) gives every sieving warp the same share, no atomics
+    if ((uint32_t)tid < 32u * kSieveWarps) {
         const uint32_t warp = (uint32_t)tid >> 5;
         const uint32_t k0 = __ldg(ms.off + warp), k1 = __ldg(ms.off + warp + 1);
         for (uint32_t k = k0; k < k1; ++k) {
@@ -863,8 +871,8 @@ extern __shared__ uint32_t g_win[];
 struct Shared6 {
     uint32_t hist[kHistSmem];          // bins by prime index (runtime loop, fallback, specials)
     uint32_t histc[3][kK];             // unrolled candidates, by class table index
-    uint32_t next_round;
-    uint32_t ns;
+    uint32_t next_round[2];            // per window slot
+    uint32_t ns[2];
     uint32_t q_base;      // word offset of the queues in dynamic shared memory
 };
 
@@ -874,7 +882,7 @@ __device__ __forceinline__ uint32_t *sh_qU(const Shared6 &sh, int warp)
 }
 __device__ __forceinline__ uint16_t *sh_qli(const Shared6 &sh, int warp)
 {
-    return (uint16_t *)(g_win + sh.q_base + (kThreads / 32) * kQueue) + (uint32_t)warp * kQueue;
+    return (uint16_t *)(g_win + sh.q_base + kMarkWarps * kQueue) + (uint32_t)warp * kQueue;
 }
 
 template <int A, bool DUMP, bool UNROLL>
@@ -987,6 +995,55 @@ __device__ __forceinline__ void flush_queue(int cls, Shared6 &sh, uint32_t &qn, 
     else ClassWork<4, DUMP, UNROLL>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
 }
 
+// marking of one tile: rounds of 32 kW words of one class, handed out dynamically
+// (class-major) through the shared counter `next_round`; qwarp indexes the
+// survivor queue of this warp
+template <bool DUMP, bool UNROLL>
+__device__ __forceinline__ void mark_tile(Shared6 &sh, uint32_t &next_round, uint64_t u0, uint32_t tw,
+                                          const uint32_t *wA, const uint32_t *wB, uint32_t halo,
+                                          const VerifyArgs &a, Acc &acc, uint32_t &best_p, int lane, int qwarp)
+{
+    const uint32_t r1 = (tw + 32 * kW - 1) / (32 * kW);
+    uint32_t qn = 0;
+    int qcls = 0;
+    while (true) {
+        uint32_t r = 0;
+        if (lane == 0) r = atomicAdd(&next_round, 1u);
+        r = __shfl_sync(FULL, r, 0);
+        if (r >= 3 * r1) break;
+        const int cls = (int)(r / r1);
+        const uint32_t pair = r - (uint32_t)cls * r1;
+        if (cls != qcls) {
+            flush_queue<DUMP, UNROLL>(qcls, sh, qn, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+            qcls = cls;
+        }
+        if (cls == 0) ClassWork<0, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+        else if (cls == 1) ClassWork<2, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+        else ClassWork<4, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+    }
+    flush_queue<DUMP, UNROLL>(qcls, sh, qn, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+}
+
+// shared histograms -> result vector (all threads; callers barrier around it)
+__device__ __forceinline__ void flush_hist(Shared6 &sh, const VerifyArgs &a, int tid)
+{
+    unsigned long long *R = (unsigned long long *)a.result;
+    for (int i = tid; i < kHistSmem; i += kThreads) {
+        const uint32_t v = sh.hist[i];
+        if (v) {
+            atomicAdd(R + GB_R_HIST + i, (unsigned long long)v);
+            sh.hist[i] = 0;
+        }
+    }
+    for (int i = tid; i < 3 * kK; i += kThreads) {
+        const uint32_t v = (&sh.histc[0][0])[i];
+        if (v) {
+            atomicAdd(R + GB_R_HIST + c_tab[i / kK].bin[i % kK], (unsigned long long)v);
+            (&sh.histc[0][0])[i] = 0;
+        }
+    }
+}
+
 // UNROLL: every unrolled candidate of the three class tables is <= p_max.
 template <bool DUMP, bool UNROLL>
 // __grid_constant__: the cold out-of-line paths take `a` by reference; without it
@@ -999,13 +1056,12 @@ template <bool DUMP, bool UNROLL>
 #endif
 __global__ void __launch_bounds__(kThreads) verify_kernel(GB_PARAM)
 {
-    uint32_t *win = g_win;                     // class A window | class B window | queues
+    uint32_t *win = g_win;                     // slot windows (class A | class B) | queues
     __shared__ Shared6 sh;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t halo = a.halo;
     const uint32_t nw_max = halo + a.tile_words + kWinSlack;
-    uint32_t *wA = win, *wB = win + nw_max;
-    if (tid == 0) sh.q_base = 2 * nw_max;
+    if (tid == 0) sh.q_base = kSlots * 2 * nw_max;
     for (int i = tid; i < kHistSmem; i += kThreads) sh.hist[i] = 0;
     for (int i = tid; i < 3 * kK; i += kThreads) (&sh.histc[0][0])[i] = 0;
     Acc acc;
@@ -1021,91 +1077,79 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(GB_PARAM)
     cy.n_steady = 0;
     cy.tile_m = 32 * a.tile_words;
     uint32_t ns_run = 0;                       // thread 0: running steady count (monotone)
+    const MedSched med{a.med_idx, a.med_off};
 
+#if GB_WS
+    // Warp-specialized pipeline: at step s the sieving warps (0 .. kSieveWarps-1)
+    // build tile s in slot s%2 while the marking warps consume tile s-1 from the
+    // other slot; one CTA barrier per step.
+    constexpr int kNS = 32 * kSieveWarps;
+    const bool sieving = warp < kSieveWarps;
+    const uint64_t n_my = t_end - t_begin;
+    for (uint64_t st = 0; st <= n_my; ++st) {
+        if (sieving) {
+            if (st < n_my) {
+                const int slot = (int)(st & 1);
+                const uint64_t u0 = a.u_first + (t_begin + st) * a.tile_words;
+                const uint32_t tw = (uint32_t)min((uint64_t)a.tile_words, a.u_end - u0);
+                const int64_t g0 = (int64_t)u0 - (int64_t)halo;
+                uint32_t *wA = win + slot * 2 * nw_max, *wB = wA + nw_max;
+                if (tid == 0) {
+                    sh.ns[slot] = steady_count(cy, g0, a.sp, ns_run);
+                    sh.next_round[slot] = 0;
+                }
+                group_sync<kNS>();
+                cy.n_steady = sh.ns[slot];
+                if (cy.tile_m == kTileM)
+                    sieve6_window<true, kNS>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask,
+                                             a.lmask_g0, a.lmask_stride, tid);
+                else
+                    sieve6_window<false, kNS>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask,
+                                              a.lmask_g0, a.lmask_stride, tid);
+                cy.have_prev = true;
+            }
+        } else if (st >= 1) {
+            const int slot = (int)((st - 1) & 1);
+            const uint64_t u0 = a.u_first + (t_begin + st - 1) * a.tile_words;
+            const uint32_t tw = (uint32_t)min((uint64_t)a.tile_words, a.u_end - u0);
+            const uint32_t *wA = win + slot * 2 * nw_max, *wB = wA + nw_max;
+            mark_tile<DUMP, UNROLL>(sh, sh.next_round[slot], u0, tw, wA, wB, halo, a, acc, best_p, lane,
+                                    warp - kSieveWarps);
+        }
+        __syncthreads();
+        // periodic flush of the shared histograms keeps their 32-bit bins exact
+        if ((st & 63) == 63 || st == n_my) {
+            flush_hist(sh, a, tid);
+            __syncthreads();
+        }
+    }
+#else
     for (uint64_t tile = t_begin; tile < t_end; ++tile) {
         const uint64_t u0 = a.u_first + tile * a.tile_words;
         const uint32_t tw = (uint32_t)min((uint64_t)a.tile_words, a.u_end - u0);
         const int64_t g0 = (int64_t)u0 - (int64_t)halo;
+        uint32_t *wA = win, *wB = win + nw_max;
         __syncthreads();                      // previous tile fully consumed
         if (tid == 0) {
-            sh.next_round = 0;
-            sh.ns = steady_count(cy, g0, a.sp, ns_run);
+            sh.next_round[0] = 0;
+            sh.ns[0] = steady_count(cy, g0, a.sp, ns_run);
         }
         __syncthreads();
-#ifdef GB_PROFILE_PHASES
-        const long long t0 = clock64();
-#endif
-        cy.n_steady = sh.ns;
+        cy.n_steady = sh.ns[0];
         if (cy.tile_m == kTileM)
-            sieve6_window<true>(wA, wB, g0, halo + tw, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2, a.i_b1,
-                                a.lmask, a.lmask_g0, a.lmask_stride);
+            sieve6_window<true, kThreads>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask,
+                                          a.lmask_g0, a.lmask_stride, tid);
         else
-            sieve6_window<false>(wA, wB, g0, halo + tw, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2, a.i_b1,
-                                 a.lmask, a.lmask_g0, a.lmask_stride);
+            sieve6_window<false, kThreads>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask,
+                                           a.lmask_g0, a.lmask_stride, tid);
         cy.have_prev = true;
-#ifdef GB_PROFILE_PHASES
-        const long long t1 = clock64();
-#endif
         __syncthreads();
-#ifdef GB_PROFILE_PHASES
-        const long long t2 = clock64();
-#endif
-
-        // marking: rounds of 64 words of one class, handed out dynamically (class-major)
-        const uint32_t r1 = (tw + 32 * kW - 1) / (32 * kW);
-        uint32_t qn = 0;
-        int qcls = 0;
-        while (true) {
-            uint32_t r = 0;
-            if (lane == 0) r = atomicAdd(&sh.next_round, 1u);
-            r = __shfl_sync(FULL, r, 0);
-            if (r >= 3 * r1) break;
-            const int cls = (int)(r / r1);
-            const uint32_t pair = r - (uint32_t)cls * r1;
-            if (cls != qcls) {
-                flush_queue<DUMP, UNROLL>(qcls, sh, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
-                qcls = cls;
-            }
-            if (cls == 0) ClassWork<0, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, warp);
-            else if (cls == 1) ClassWork<2, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, warp);
-            else ClassWork<4, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, warp);
-        }
-        flush_queue<DUMP, UNROLL>(qcls, sh, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
-#ifdef GB_PROFILE_PHASES
-        const long long t3 = clock64();
-#endif
-
+        mark_tile<DUMP, UNROLL>(sh, sh.next_round[0], u0, tw, wA, wB, halo, a, acc, best_p, lane, warp);
         // per-tile flush of the shared histograms keeps their 32-bit bins exact
         __syncthreads();
-#ifdef GB_PROFILE_PHASES
-        const long long t4 = clock64();
-        if (lane == 0) {
-            atomicAdd(&g_prof[0], (unsigned long long)(t1 - t0));   // sieve (per warp)
-            atomicAdd(&g_prof[1], (unsigned long long)(t2 - t1));   // wait after sieve
-            atomicAdd(&g_prof[2], (unsigned long long)(t3 - t2));   // mark
-            atomicAdd(&g_prof[3], (unsigned long long)(t4 - t3));   // wait after mark
-            atomicAdd(&g_prof[4], 1ull);
-        }
-        if (blockIdx.x == 0 && tid == 0 && tile + 1 == t_end)
-            printf("GBPROF sieve=%llu sieve_wait=%llu mark=%llu mark_wait=%llu warp-tiles=%llu\n", g_prof[0],
-                   g_prof[1], g_prof[2], g_prof[3], g_prof[4]);
-#endif
-        unsigned long long *R = (unsigned long long *)a.result;
-        for (int i = tid; i < kHistSmem; i += kThreads) {
-            const uint32_t v = sh.hist[i];
-            if (v) {
-                atomicAdd(R + GB_R_HIST + i, (unsigned long long)v);
-                sh.hist[i] = 0;
-            }
-        }
-        for (int i = tid; i < 3 * kK; i += kThreads) {
-            const uint32_t v = (&sh.histc[0][0])[i];
-            if (v) {
-                atomicAdd(R + GB_R_HIST + c_tab[i / kK].bin[i % kK], (unsigned long long)v);
-                (&sh.histc[0][0])[i] = 0;
-            }
-        }
+        flush_hist(sh, a, tid);
     }
+#endif
     acc.verified = acc.evens - acc.unres;
 
     // flush: warp-reduce then one atomic per warp per field
@@ -1176,11 +1220,11 @@ __global__ void __launch_bounds__(kThreads) sieve_out_kernel(const __grid_consta
         __syncthreads();
         cy.n_steady = sh_ns;
         if (cy.tile_m == kTileM)
-            sieve6_window<true>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
-                                a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride);
+            sieve6_window<true, kThreads>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off},
+                                          a.i_b2, a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride, tid);
         else
-            sieve6_window<false>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
-                                 a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride);
+            sieve6_window<false, kThreads>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off},
+                                           a.i_b2, a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride, tid);
         cy.have_prev = true;
         __syncthreads();
         for (uint32_t i = tid; i < tw; i += kThreads) {
