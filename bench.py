@@ -42,9 +42,10 @@ def parse():
                     help="c4: every even n in [4, N] (the metric's workload); c5: the window "
                          "[4e18 - 1e11, 4e18) of BASELINE.json configs[4]")
     ap.add_argument("--p-max", type=int, default=65521)
-    ap.add_argument("--mode", default="bulk", choices=["bulk", "pern"],
+    ap.add_argument("--mode", default="bulk", choices=["bulk", "pern", "resident"],
                     help="bulk: the product path (inverted bulk marking); pern: the paper's per-n "
-                         "gpu3 kernel (NEXT-1 comparison, PAPER.md:82-95)")
+                         "gpu3 kernel (NEXT-1, PAPER.md:82-95); resident: the paper's gpu2 with the "
+                         "whole odd bitset of [3, hi) sieved into HBM each step (NEXT-2, PAPER.md:41-59)")
     ap.add_argument("--strips-per-rank", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -187,8 +188,20 @@ def main():
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(4 * l2_bytes, 1 << 28) // 4, dtype=torch.int32, device=dev)
 
+    bits = None
+    if args.mode == "resident":
+        n_bits_words = (hi - 3) // 128 + 1
+        bits = torch.empty(n_bits_words, dtype=torch.int64, device=dev)
+
     def step(k_events=None):
         r = V.new_result()
+        if bits is not None:                         # gpu2: sieve [3, hi) into HBM, then per-n lookups
+            gb.gb_sieve_segment(V.ctx, 0, bits.numel(), bits, stream)
+            for a, b in strips:
+                gb.gb_verify_range_resident(V.ctx, a, b, args.p_max, bits, bits.numel(), r, None, stream)
+            V.finalize(r)
+            gdist.reduce_result(r)
+            return r
         for a, b in strips:
             if k_events is not None:
                 e0 = torch.cuda.Event(enable_timing=True)
@@ -273,7 +286,7 @@ def main():
     evens_per_launch = evens / max(1, len(strips) * world)
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     alu_peak = 148 * 64 * sm_mhz * 1e6 / 1e12           # T int32 lane-ops/s on the ALU pipe
-    achieved = ops_per_even * evens_per_launch / avg_launch_s / 1e12
+    achieved = ops_per_even * evens_per_launch / avg_launch_s / 1e12 if n_launch else None
     traffic, traffic_src = None, None
     try:   # DRAM bytes per even n of verify_kernel from the latest committed ncu --set full capture
         import glob
@@ -285,13 +298,13 @@ def main():
     except Exception:
         pass
     roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Tops/s",
-                "frac": achieved / alu_peak, "traffic": traffic,
+                "frac": achieved / alu_peak if achieved else None, "traffic": traffic,
                 "traffic_note": (f"DRAM read+write bytes per launch, scaled per even n from {traffic_src}"
                                  if traffic_src else None),
                 "kernel": "verify_kernel (fused sieve + mark + fallback)",
                 "ops_per_even": ops_per_even,
                 "peak_basis": f"148 SM x 64 int32 lanes/clk (ALU pipe) x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
-                "kernel_ms_per_launch": avg_launch_s * 1e3, "launches_timed": n_launch,
+                "kernel_ms_per_launch": avg_launch_s * 1e3 if n_launch else None, "launches_timed": n_launch,
                 "kernel_share_of_step": box_kern_ms / box_ms if box_ms else None}
 
     # ---- sieve GB/s (BASELINE.json metric, second half): standalone gb_sieve_segment

@@ -172,6 +172,24 @@ gb_status gb_verify_range_host(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p
 gb_status gb_verify_range_pern(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_max,
                                int64_t *d_result, uint32_t *d_pmin_dump, void *stream);
 
+/* NEXT-2 comparison mode: the paper's gpu2 (PAPER.md:41-59,
+ * section 2.2, "Global GPU-Resident Bitset") -- the odd bitset of the WHOLE range is
+ * resident in HBM (d_bits: words [0, n_words) of the global layout, caller-owned,
+ * e.g. written by gb_sieve_segment; 62.5 GB at N = 1e12 fits a B200), and one thread
+ * per even n scans odd p <= p_max ascending with a direct bitset lookup of q.
+ * Requires 3 + 128 * n_words >= hi (GB_EINVAL otherwise).  Same result semantics
+ * as gb_verify_range; one launch. */
+gb_status gb_verify_range_resident(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_max,
+                                   const uint64_t *d_bits, uint64_t n_words, int64_t *d_result,
+                                   uint32_t *d_pmin_dump, void *stream);
+
+/* NEXT-3: single_check (section 2.4) for ONE even n, 4 <= n <
+ * 2^64: writes to *d_out (device u64) the minimal prime p <= p_limit with n - p
+ * prime (p tested by the resident bitset or MR64; q = n - p likewise), 0 if none.
+ * The paper's tool returns some valid partition; this one returns the minimal one.
+ * GB_EINVAL for odd n, n < 4, misaligned d_out. */
+gb_status gb_single_check(gb_ctx *ctx, uint64_t n, uint64_t p_limit, uint64_t *d_out, void *stream);
+
 /* Deterministic 64-bit Miller-Rabin (12 prime bases 2..37; PAPER.md:89,
  * SPEC.md:128) as used by the fallback: d_out[i] = 1 iff d_x[i] is prime. */
 gb_status gb_is_prime_u64(const uint64_t *d_x, uint8_t *d_out, uint64_t n, void *stream);

@@ -576,6 +576,49 @@ gb_status gb_verify_range_pern(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p
     return GB_OK;
 }
 
+gb_status gb_verify_range_resident(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_max, const uint64_t *d_bits,
+                                   uint64_t n_words, int64_t *d_result, uint32_t *d_pmin_dump, void *stream)
+{
+    if (!ctx || !d_result || !d_bits || ((uintptr_t)d_result & 7) || ((uintptr_t)d_bits & 7) ||
+        ((uintptr_t)d_pmin_dump & 3))
+        return GB_EINVAL;
+    if (lo > hi || hi > GB_HI_LIMIT || p_max < 3 || p_max > ctx->p_max) return GB_EINVAL;
+    const uint64_t lo_e = lo < 4 ? 4 : lo + (lo & 1);
+    if (hi <= lo_e) return GB_OK;
+    if (hi > ctx->hi_max) return GB_ERANGE;
+    if (lo_e < ctx->origin || ((hi - ctx->origin) >> 1) >= (1ull << GB_KEY_SHIFT)) return GB_EINVAL;
+    if (n_words > (1ull << 58) || 3 + 128 * n_words < hi) return GB_EINVAL;   // every odd q < hi resident
+    const uint32_t n_cand = count_le(ctx->h_primes, p_max);
+    if (n_cand == 0) return GB_EINVAL;
+    DeviceGuard g(ctx->device);
+    PerNArgs a;
+    a.n_first = lo_e;
+    a.n_evens = (hi - lo_e + 1) / 2;
+    a.n_cand = n_cand;
+    a.primes = ctx->primes;
+    a.n_base = (uint32_t)ctx->n_base;
+    a.base_bits = ctx->bits;
+    a.R = ctx->R;
+    a.seg_bits = d_bits;               // the whole range's bitset is the "segment"
+    a.seg_word_lo = 0;
+    a.seg_q_lo = 3;
+    a.seg_q_hi = 3 + 128 * n_words;
+    a.p_fallback = (uint64_t)ctx->h_primes[n_cand - 1] + 2;
+    a.cap = UINT64_MAX;
+    a.origin = ctx->origin;
+    a.lo_e = lo_e;
+    a.result = d_result;
+    a.dump = d_pmin_dump;
+    return launch_pern(a, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
+}
+
+gb_status gb_single_check(gb_ctx *ctx, uint64_t n, uint64_t p_limit, uint64_t *d_out, void *stream)
+{
+    if (!ctx || !d_out || ((uintptr_t)d_out & 7) || n < 4 || (n & 1)) return GB_EINVAL;
+    DeviceGuard g(ctx->device);
+    return launch_single_check(n, p_limit, ctx->bits, ctx->R, d_out, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
+}
+
 gb_status gb_is_prime_u64(const uint64_t *d_x, uint8_t *d_out, uint64_t n, void *stream)
 {
     if (n && (!d_x || !d_out || ((uintptr_t)d_x & 7))) return GB_EINVAL;

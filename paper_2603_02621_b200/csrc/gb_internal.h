@@ -161,6 +161,8 @@ struct PerNArgs {
     uint32_t *dump;
 };
 cudaError_t launch_pern(const PerNArgs &a, cudaStream_t st);
+cudaError_t launch_single_check(uint64_t n, uint64_t p_limit, const uint64_t *bits, uint64_t R, uint64_t *out,
+                                cudaStream_t st);
 
 // Launchers (gb_kernels.cu).  Each returns the cudaGetLastError() of its launch.
 cudaError_t launch_seed(uint64_t s, uint32_t *primes, uint64_t *magic, uint4 *pk,

@@ -153,3 +153,45 @@ cudaError_t launch_pern(const PerNArgs &a, cudaStream_t st)
 }
 
 }  // namespace gb
+
+namespace gb {
+
+// ---------------------------------------------------------------------------
+// NEXT-3: single_check (section 2.4): the minimal prime p with
+// n - p prime for ONE even n < 2^64.  One 1024-thread CTA scans odd candidates in
+// batches of 1024 ascending (p tested by the resident bitset, or MR64 above R;
+// q = n - p likewise) and stops at the first batch with a hit; the block minimum
+// of that batch is p_min (the paper's variant returns any valid p; this one is
+// minimal).  n = 4 -> 2.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) single_check_kernel(uint64_t n, uint64_t p_limit, const uint64_t *bits,
+                                                            uint64_t R, uint64_t *out)
+{
+    __shared__ unsigned long long best;
+    if (threadIdx.x == 0) best = ~0ull;
+    __syncthreads();
+    if (n == 4) {
+        if (threadIdx.x == 0) *out = p_limit >= 2 ? 2 : 0;
+        return;
+    }
+    const uint64_t half = n / 2;
+    const uint64_t lim = half < p_limit ? half : p_limit;
+    for (uint64_t base = 3; base <= lim; base += 2 * blockDim.x) {
+        const uint64_t p = base + 2 * (uint64_t)threadIdx.x;
+        if (p <= lim && is_prime_dev(p, bits, R) && is_prime_dev(n - p, bits, R)) atomicMin(&best, p);
+        __syncthreads();
+        if (best != ~0ull) break;                 // block-uniform: read after the barrier
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = best == ~0ull ? 0 : best;
+}
+
+cudaError_t launch_single_check(uint64_t n, uint64_t p_limit, const uint64_t *bits, uint64_t R, uint64_t *out,
+                                cudaStream_t st)
+{
+    single_check_kernel<<<1, 1024, 0, st>>>(n, p_limit, bits, R, out);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace gb

@@ -64,6 +64,8 @@ _sigs = {
     "gb_verify_range_ex": (ctypes.c_int, [_vp, _u64, _u64, _u32, _u64, _vp, _vp, _vp]),
     "gb_verify_range_host": (ctypes.c_int, [_vp, _u64, _u64, _u32, _vp, _vp, _vp]),
     "gb_verify_range_pern": (ctypes.c_int, [_vp, _u64, _u64, _u32, _vp, _vp, _vp]),
+    "gb_verify_range_resident": (ctypes.c_int, [_vp, _u64, _u64, _u32, _vp, _u64, _vp, _vp, _vp]),
+    "gb_single_check": (ctypes.c_int, [_vp, _u64, _u64, _vp, _vp]),
     "gb_is_prime_u64": (ctypes.c_int, [_vp, _vp, _u64, _vp]),
     "gb_launch_count": (_u64, []),
     "gb_status_string": (ctypes.c_char_p, [ctypes.c_int]),
@@ -141,6 +143,16 @@ def gb_verify_range(ctx: int, lo: int, hi: int, p_max: int, d_result, d_dump, st
 def gb_verify_range_pern(ctx: int, lo: int, hi: int, p_max: int, d_result, d_dump, stream) -> None:
     _check(_lib.gb_verify_range_pern(ctx, lo, hi, p_max, _ptr(d_result), _ptr(d_dump), _ptr_stream(stream)),
            "gb_verify_range_pern")
+
+
+def gb_verify_range_resident(ctx: int, lo: int, hi: int, p_max: int, d_bits, n_words: int, d_result, d_dump,
+                             stream) -> None:
+    _check(_lib.gb_verify_range_resident(ctx, lo, hi, p_max, _ptr(d_bits), n_words, _ptr(d_result), _ptr(d_dump),
+                                         _ptr_stream(stream)), "gb_verify_range_resident")
+
+
+def gb_single_check(ctx: int, n: int, p_limit: int, d_out, stream) -> None:
+    _check(_lib.gb_single_check(ctx, n, p_limit, _ptr(d_out), _ptr_stream(stream)), "gb_single_check")
 
 
 def gb_verify_range_ex(ctx: int, lo: int, hi: int, p_max: int, cap: int, d_result, d_dump,

@@ -68,6 +68,27 @@ class Verifier:
         self.stream.synchronize()
         return self.decode(r), d
 
+    def run_resident(self, lo: int, hi: int, bits: torch.Tensor, p_max: int | None = None, dump: bool = False):
+        """NEXT-2: gpu2-style verification against a resident odd bitset `bits`
+        (int64 words [0, n) of the global layout, e.g. sieve_segment(0, n))."""
+        r = self.new_result()
+        d = None
+        if dump:
+            e = 4 if lo < 4 else lo + (lo & 1)
+            d = torch.zeros(max(0, (hi - e + 1) // 2), dtype=torch.int32, device=self.device)
+        gb.gb_verify_range_resident(self.ctx, lo, hi, self.p_max if p_max is None else p_max, bits, bits.numel(), r,
+                                    d if (d is not None and d.numel()) else None, self.stream)
+        self.finalize(r)
+        self.stream.synchronize()
+        return self.decode(r), d
+
+    def single_check(self, n: int, p_limit: int = (1 << 64) - 1) -> int:
+        """NEXT-3: minimal p <= p_limit with n - p prime for one even n (0 if none)."""
+        out = torch.zeros(1, dtype=torch.int64, device=self.device)
+        gb.gb_single_check(self.ctx, n, p_limit, out, self.stream)
+        self.stream.synchronize()
+        return int(out.cpu()[0]) & ((1 << 64) - 1)
+
     def sieve_segment(self, word_lo: int, n_words: int) -> torch.Tensor:
         out = torch.empty(n_words, dtype=torch.int64, device=self.device)
         gb.gb_sieve_segment(self.ctx, word_lo, n_words, out, self.stream)
