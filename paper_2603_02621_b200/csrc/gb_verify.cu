@@ -133,16 +133,19 @@ __host__ __device__ constexpr uint32_t inv6(uint32_t p) { return p % 6 == 1 ? (5
 __host__ __device__ constexpr uint32_t rA_of(uint32_t p) { return p - inv6(p); }
 __host__ __device__ constexpr uint32_t rB_of(uint32_t p) { return (5 * rA_of(p)) % p; }
 
-// first hit (local offset from m_lo) of the progression m == r (mod p), m >= (p^2-1)/6
-__device__ __forceinline__ uint64_t first_hit6(uint32_t p, uint32_t r, uint64_t magic, int64_t m_lo,
-                                               int64_t m_hi)
+// first hits (local offsets from m_lo) of the progressions m == rA, rB (mod p) with
+// m >= (p^2-1)/6 (the first multiple cleared is p^2), 0xFFFFFFFF if p^2 is beyond
+// the window; both classes share the start ms and its residue (one modulo)
+__device__ __forceinline__ void first_hits6(uint32_t p, uint32_t rA, uint32_t rB, uint64_t magic, int64_t m_lo,
+                                            int64_t m_hi, uint32_t &oa, uint32_t &ob)
 {
     const int64_t mmin = (int64_t)(((uint64_t)p * p - 1) / 6);
-    if (mmin >= m_hi) return UINT64_MAX;
+    if (mmin >= m_hi) { oa = ob = 0xFFFFFFFFu; return; }
     const uint64_t ms = (uint64_t)(mmin > m_lo ? mmin : m_lo);
     const uint32_t rem = mod_magic(ms, p, magic);
-    const uint32_t delta = r >= rem ? r - rem : r + p - rem;
-    return ms + delta - (uint64_t)m_lo;
+    const uint64_t base = ms - (uint64_t)m_lo;
+    oa = (uint32_t)(base + (rA >= rem ? rA - rem : rA + p - rem));
+    ob = (uint32_t)(base + (rB >= rem ? rB - rem : rB + p - rem));
 }
 
 // next tile's first hit (the window moves up by tile_m)
@@ -315,8 +318,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
                     ob = cy->off[cy->stride + pi];
                 } else {
                     const uint64_t mg = __ldg(sp.magic + pi);
-                    oa = (uint32_t)first_hit6(k.x, k.z, mg, m_lo, m_hi);
-                    ob = (uint32_t)first_hit6(k.x, k.w, mg, m_lo, m_hi);
+                    first_hits6(k.x, k.z, k.w, mg, m_lo, m_hi, oa, ob);
                 }
                 if (carried) {
                     const uint32_t tm = tile_mod<DEF_TILE>(cy, k);
@@ -466,8 +468,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             ob = cy->off[cy->stride + pi];
         } else {
             const uint64_t mg = __ldg(sp.magic + pi);
-            oa = (uint32_t)first_hit6(k.x, k.z, mg, m_lo, m_hi);
-            ob = (uint32_t)first_hit6(k.x, k.w, mg, m_lo, m_hi);
+            first_hits6(k.x, k.z, k.w, mg, m_lo, m_hi, oa, ob);
         }
         for (uint32_t b = oa; b < nbits; b += k.x) clear_bit(sA, b);
         for (uint32_t b = ob; b < nbits; b += k.x) clear_bit(sB, b);
