@@ -117,6 +117,7 @@ struct Carry6 {
     uint64_t stride;
     uint32_t n_carry;
     uint32_t n_steady;        // primes [i_med, n_steady): carried, p^2 <= 6 m_lo + 1
+    bool init;                // first tile of a run: fill the carry row for [i_med, n_steady) first
     uint32_t tile_m;          // m-span of a tile (window step); kTileM unless p_max forces a smaller tile
     bool have_prev;
 };
@@ -238,6 +239,19 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
     const uint32_t lane = (uint32_t)tid & 31;
     constexpr int nt = NT;
     const uint32_t sA = smem_addr(wA), sB = smem_addr(wB);
+    if (cy->init) {
+        // first tile of this CTA's run: carried offsets of the steady primes by modulo
+        const int64_t m_lo0 = g0 * 32, m_hi0 = (g0 + (int64_t)nw) * 32;
+        const uint64_t ipol = carry_policy();
+        for (uint32_t pi = sp.i_med + tid; pi < cy->n_steady; pi += nt) {
+            const uint4 k = __ldg(sp.pk + pi);
+            uint32_t oa, ob;
+            first_hits6(k.x, k.z, k.w, __ldg(sp.magic + pi), m_lo0, m_hi0, oa, ob);
+            carry_st(cy->off + pi, oa, ipol);
+            carry_st(cy->off + cy->stride + pi, ob, ipol);
+        }
+        group_sync<NT>();
+    }
     // Phase T: primes 5..31 by shifted word patterns, per-thread incremental phases
     {
         int64_t g = g0 + tid;
@@ -834,15 +848,18 @@ __device__ __forceinline__ uint32_t take_special(uint32_t U, uint64_t u, uint32_
     return U;
 }
 
-// Steady primes of the window starting at class word g0 (thread 0): carried (the
-// previous tile was done by this CTA) and p^2 <= 6 m_lo + 1, i.e. the progression
-// started below the window.  ns_run: the running (monotone) count of this CTA.
+// Steady primes of the window starting at class word g0 (thread 0): carried and
+// p^2 <= 6 m_lo + 1, i.e. the progression started below the window.  If the
+// previous tile was not done by this CTA (first tile of its run or of a K-LARGE
+// chunk) bit 31 asks sieve6_window to compute their offsets into the carry row
+// first, so every such prime still takes the balanced steady loops.  ns_run: the
+// running (monotone) count of this CTA.
 __device__ __forceinline__ uint32_t steady_count(const Carry6 &cy, int64_t g0, const SievePrimes &sp,
                                                  uint32_t &ns_run)
 {
     uint32_t ns = 0;
     const int64_t m_lo = g0 * 32;
-    if (cy.have_prev && m_lo > 0) {
+    if (m_lo > 0) {
         const uint64_t lim = 6 * (uint64_t)m_lo + 1;
         const uint32_t top = min(cy.n_carry, sp.n_use);
         ns = max(ns_run, sp.i_med);
@@ -863,7 +880,8 @@ __device__ __forceinline__ uint32_t steady_count(const Carry6 &cy, int64_t g0, c
         }
         ns_run = ns;
     }
-    return ns;
+    // bit 31: the previous tile was not done here, the carry row must be filled first
+    return ns | (cy.have_prev || ns <= sp.i_med ? 0u : 0x80000000u);
 }
 
 // dynamic shared memory: class A window | class B window | per-warp survivor queues
@@ -1076,6 +1094,7 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(GB_PARAM)
     cy.n_carry = a.n_carry;
     cy.have_prev = false;
     cy.n_steady = 0;
+    cy.init = false;
     cy.tile_m = 32 * a.tile_words;
     uint32_t ns_run = 0;                       // thread 0: running steady count (monotone)
     const MedSched med{a.med_idx, a.med_off};
@@ -1100,7 +1119,8 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(GB_PARAM)
                     sh.next_round[slot] = 0;
                 }
                 group_sync<kNS>();
-                cy.n_steady = sh.ns[slot];
+                cy.n_steady = sh.ns[slot] & 0x7FFFFFFFu;
+                cy.init = sh.ns[slot] >> 31;
                 if (cy.tile_m == kTileM)
                     sieve6_window<true, kNS>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask,
                                              a.lmask_g0, a.lmask_stride, tid);
@@ -1136,7 +1156,8 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(GB_PARAM)
             sh.ns[0] = steady_count(cy, g0, a.sp, ns_run);
         }
         __syncthreads();
-        cy.n_steady = sh.ns[0];
+        cy.n_steady = sh.ns[0] & 0x7FFFFFFFu;
+        cy.init = sh.ns[0] >> 31;
         if (cy.tile_m == kTileM)
             sieve6_window<true, kThreads>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask,
                                           a.lmask_g0, a.lmask_stride, tid);
@@ -1211,6 +1232,7 @@ __global__ void __launch_bounds__(kThreads) sieve_out_kernel(const __grid_consta
     cy.n_carry = a.n_carry;
     cy.have_prev = false;
     cy.n_steady = 0;
+    cy.init = false;
     cy.tile_m = 32 * a.tile_words;
     uint32_t ns_run = 0;
     for (uint64_t tile = t_begin; tile < t_end; ++tile) {
@@ -1219,7 +1241,8 @@ __global__ void __launch_bounds__(kThreads) sieve_out_kernel(const __grid_consta
         __syncthreads();                      // previous tile written out
         if (tid == 0) sh_ns = steady_count(cy, (int64_t)g0, a.sp, ns_run);
         __syncthreads();
-        cy.n_steady = sh_ns;
+        cy.n_steady = sh_ns & 0x7FFFFFFFu;
+        cy.init = sh_ns >> 31;
         if (cy.tile_m == kTileM)
             sieve6_window<true, kThreads>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off},
                                           a.i_b2, a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride, tid);
