@@ -47,7 +47,7 @@ __host__ __device__ constexpr Trans trans(int a, uint32_t p)
 }
 
 #ifndef GB_K6
-#define GB_K6 160
+#define GB_K6 192
 #endif
 #ifndef GB_P1
 #define GB_P1 56
