@@ -76,8 +76,10 @@ typedef struct gb_ctx gb_ctx;   /* opaque; host object owned by libgb */
 
 /* Largest p_max accepted (the fast-path prime bound, PAPER.md:173 P_SMALL = 1e6). */
 #define GB_PMAX_LIMIT 1048576u
-/* Largest hi accepted (room for halos and carries). */
-#define GB_HI_LIMIT 18446744073708503040ull   /* 2^64 - 2^20 */
+/* Largest hi accepted: 2^62 (4.61e18, above BASELINE.json's 4e18 window).  Every n
+ * stays below 2^63, so GB_R_FIRST_UNRESOLVED_N (an int64 MIN) and the int64 n
+ * fields of the result are exact, and 6m + 5, p*k, halos and carries cannot wrap. */
+#define GB_HI_LIMIT 4611686018427387904ull   /* 2^62 */
 
 /* Bytes of device workspace a ctx needs for ranges with hi <= hi_max and fast
  * path bound p_max (base-prime bitset + list + per-prime constants + scratch).

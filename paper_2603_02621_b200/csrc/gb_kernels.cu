@@ -450,9 +450,11 @@ __global__ void __launch_bounds__(kLargeBlock) large_mark_wheel_kernel(LargeArgs
     __syncthreads();
     const int64_t m_lo = a.g0 * 32;
     const uint32_t nbits = 32 * a.nw;
-    const int64_t q_base = 6 * m_lo;                       // offsets: off = q - q_base, m = off / 6
+    // offsets off = q - q_base, m = off / 6; q_base = 6 m_lo wraps mod 2^64 when
+    // m_lo < 0 (ranges starting below the halo), and exceeds INT64_MAX near 2^64
+    const uint64_t q_base = 6 * (uint64_t)m_lo;
     const uint64_t lim_off = 6ull * nbits;                 // < 2^32 (nbits < 2^30 / 3)
-    const uint64_t q_first = q_base > 0 ? (uint64_t)q_base : 0;
+    const uint64_t q_first = m_lo > 0 ? q_base : 0;
     const uint64_t n = a.i_end - a.i_begin;
     const uint64_t total = (uint64_t)gridDim.x * blockDim.x;
     uint32_t *__restrict__ mA = a.mask;
@@ -478,7 +480,7 @@ __global__ void __launch_bounds__(kLargeBlock) large_mark_wheel_kernel(LargeArgs
         const uint32_t adv = s_res[idx0] - kr;
         k += adv;
         uint32_t idx = idx0;
-        uint64_t off = p * k - (uint64_t)q_base;
+        uint64_t off = p * k - q_base;
         if (off >= lim_off) continue;
         const uint32_t kk = km + adv;                     // k mod kM, possibly + up to 10
         uint32_t r11 = kk % 11, r13 = kk % 13, r17 = kk % 17, r19 = kk % 19;
