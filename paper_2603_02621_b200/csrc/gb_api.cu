@@ -335,7 +335,9 @@ gb_status gb_sieve_segment(gb_ctx *ctx, uint64_t word_lo, uint64_t n_words, uint
     a.lmask = nullptr;
     a.lmask_g0 = 0;
     a.lmask_stride = 0;
-    const size_t smem = 2 * 4ull * (a.tile_words + 1 + kWinSlackWords);
+    // two class windows + the TMA staging ring of base-prime tiles (2 x 1024 x 16 B;
+    // used by the GB_SIEVE_STAGED build)
+    const size_t smem = 4ull * ((2 * (a.tile_words + 1 + kWinSlackWords) + 3) & ~3ull) + 2 * 1024 * 16;
     const int grid_max = (int)std::min<uint64_t>((uint64_t)ctx->num_sms, ctx->carry_ctas);
     const uint32_t i_large = count_le(ctx->h_primes, kCarryPrimeMax);
     const bool large = a.sp.n_use > i_large;

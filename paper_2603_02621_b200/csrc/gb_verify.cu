@@ -219,6 +219,53 @@ __device__ __forceinline__ void carry_st(uint32_t *p, uint32_t v, uint64_t pol)
 #endif
 }
 
+// ---- TMA (cp.async.bulk) staging of base-prime tiles for the standalone sieve ----
+constexpr uint32_t kStagePrimes = 1024;         // primes per staged tile (16 B each): 16 KB
+constexpr uint32_t kStageBufs = 2;              // ring depth (32 KB)
+// gb_sieve_segment with TMA-staged base-prime tiles (GB_SIEVE_STAGED=1) is an A/B
+// option: parity-green (the sieve tests pass on that build) but measured slower than
+// the __ldg path with 2 primes in flight per thread -- 5.82 vs 5.31 ms per 2^34
+// integers at 1e12, 19.2 vs 18.8 ms at 4e18.
+#ifdef GB_SIEVE_STAGED
+constexpr bool kSieveStaged = true;
+#else
+constexpr bool kSieveStaged = false;
+#endif
+struct TmaStage {
+    uint4 *buf;                                 // kStageBufs x kStagePrimes (p, tile_m mod p, rA, rB)
+    uint64_t *bar;                              // kStageBufs "full" mbarriers (TMA transaction count)
+    uint32_t *done;                             // kStageBufs counters of warps done with the buffer
+    uint32_t uses[kStageBufs];                  // completed phases per buffer (parity)
+};
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// one thread: arm the barrier with the byte count and start the bulk copy global -> shared
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    uint32_t done;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                     " selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(done)
+                     : "r"(smem_addr(bar)), "r"(parity)
+                     : "memory");
+    } while (!done);
+}
+
 // barrier of the NT threads that run sieve6_window: the whole CTA, or (warp-
 // specialized verify kernel) the sieving warps 0 .. NT/32-1 on named barrier 1
 template <int NT>
@@ -230,10 +277,11 @@ __device__ __forceinline__ void group_sync()
 
 // K-SIEVE of one tile's two class windows by NT threads (gtid = 0 .. NT-1, whole
 // warps); ends WITHOUT a barrier
-template <bool DEF_TILE, int NT>
+template <bool DEF_TILE, int NT, bool STAGED = false>
 __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
                               Carry6 *cy, const MedSched &ms, uint32_t i_b2, uint32_t i_b1,
-                              const uint32_t *__restrict__ lm, int64_t lg0, uint64_t lstride, int gtid)
+                              const uint32_t *__restrict__ lm, int64_t lg0, uint64_t lstride, int gtid,
+                              TmaStage *stg = nullptr)
 {
     const int tid = gtid;
     const uint32_t lane = (uint32_t)tid & 31;
@@ -374,6 +422,52 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
 #define GB_KB 2
 #endif
     constexpr int kB = GB_KB;
+    if constexpr (STAGED) {
+        // steady primes from TMA-staged tiles of their constants (cp.async.bulk into a
+        // ring of kStageBufs shared buffers, completion on an mbarrier): thread t takes
+        // prime t of the tile, both classes, by the same three regimes as below.  The
+        // last warp done with a buffer refills it, so no CTA-wide barrier is needed.
+        static_assert(NT == kStagePrimes, "one prime per thread");
+        const uint32_t n_st = s_end - b_begin;
+        const uint32_t nch = (n_st + kStagePrimes - 1) / kStagePrimes;
+        auto issue = [&](uint32_t c) {
+            const uint32_t cnt = min(kStagePrimes, n_st - c * kStagePrimes);
+            tma_load_1d(stg->buf + (c % kStageBufs) * kStagePrimes, sp.pk + b_begin + c * kStagePrimes, 16 * cnt,
+                        stg->bar + (c % kStageBufs));
+        };
+        if (tid == 0)
+            for (uint32_t c = 0; c < kStageBufs && c < nch; ++c) issue(c);
+        for (uint32_t c = 0; c < nch; ++c) {
+            const uint32_t b = c % kStageBufs;
+            mbar_wait(stg->bar + b, stg->uses[b] & 1);
+            ++stg->uses[b];
+            const uint32_t pi = b_begin + c * kStagePrimes + (uint32_t)tid;
+            uint4 q = make_uint4(1, 0, 0, 0);
+            if (pi < s_end) q = stg->buf[b * kStagePrimes + tid];
+            __syncwarp();
+            if (lane == 0 && atomicAdd(stg->done + b, 1u) == NT / 32 - 1) {   // last warp out
+                stg->done[b] = 0;
+                if (c + kStageBufs < nch) issue(c + kStageBufs);
+            }
+            if (pi < s_end) {
+                const uint32_t p = q.x, tm = tile_mod<DEF_TILE>(cy, q);
+                const uint32_t oa = carry_ld(cA + pi, cpol), ob = carry_ld(cB + pi, cpol);
+                if (pi < b2) {                                   // >= 2 hits per class
+                    for (uint32_t bb = oa; bb < nbits; bb += p) clear_bit(sA, bb);
+                    for (uint32_t bb = ob; bb < nbits; bb += p) clear_bit(sB, bb);
+                } else {                                         // <= 2 (or <= 1) hits per class
+                    if (oa < nbits) clear_bit(sA, oa);
+                    if (ob < nbits) clear_bit(sB, ob);
+                    if (pi < b1) {
+                        if (oa + p < nbits) clear_bit(sA, oa + p);
+                        if (ob + p < nbits) clear_bit(sB, ob + p);
+                    }
+                }
+                carry_st(cA + pi, oa >= tm ? oa - tm : oa + p - tm, cpol);
+                carry_st(cB + pi, ob >= tm ? ob - tm : ob + p - tm, cpol);
+            }
+        }
+    } else {
     // steady primes with p <= full window / 2: hit loops (>= 2 hits per class)
     for (uint32_t w0 = b_begin + (tid & ~31u); w0 < b2; w0 += kB * nt) {   // warp-uniform trips
         const uint32_t p0 = w0 + lane;
@@ -470,6 +564,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
                 carry_st(cB + pi, ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm, cpol);
             }
         }
+    }
     }
     for (uint32_t pi = s_end + tid; pi < sp.n_use; pi += nt) {
         const uint4 k = __ldg(sp.pk + pi);
@@ -1218,7 +1313,22 @@ __global__ void __launch_bounds__(kThreads) sieve_out_kernel(const __grid_consta
     uint32_t *wA = win, *wB = win + nw_max;
     __shared__ uint32_t spread3[256];          // bit j of a byte -> bit 3j
     __shared__ uint32_t sh_ns;
+    __shared__ __align__(8) uint64_t stage_bar[kStageBufs];
+    __shared__ uint32_t stage_done[kStageBufs];
     const int tid = threadIdx.x;
+    // TMA staging ring of base-prime tiles after the two windows (16 B aligned)
+    TmaStage stg;
+    stg.buf = (uint4 *)(win + ((2 * nw_max + 3) & ~3u));
+    stg.bar = stage_bar;
+    stg.done = stage_done;
+    for (uint32_t b = 0; b < kStageBufs; ++b) stg.uses[b] = 0;
+    if (tid == 0) {
+        for (uint32_t b = 0; b < kStageBufs; ++b) {
+            mbar_init(stage_bar + b, 1);
+            stage_done[b] = 0;
+        }
+        mbar_fence_init();
+    }
     for (int i = tid; i < 256; i += kThreads) {
         uint32_t v = 0;
         for (int j = 0; j < 8; ++j) v |= ((i >> j) & 1u) << (3 * j);
@@ -1244,11 +1354,13 @@ __global__ void __launch_bounds__(kThreads) sieve_out_kernel(const __grid_consta
         cy.n_steady = sh_ns & 0x7FFFFFFFu;
         cy.init = sh_ns >> 31;
         if (cy.tile_m == kTileM)
-            sieve6_window<true, kThreads>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off},
-                                          a.i_b2, a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride, tid);
+            sieve6_window<true, kThreads, kSieveStaged>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy,
+                                                MedSched{a.med_idx, a.med_off}, a.i_b2, a.i_b1, a.lmask,
+                                                a.lmask_g0, a.lmask_stride, tid, &stg);
         else
-            sieve6_window<false, kThreads>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off},
-                                           a.i_b2, a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride, tid);
+            sieve6_window<false, kThreads, kSieveStaged>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy,
+                                                 MedSched{a.med_idx, a.med_off}, a.i_b2, a.i_b1, a.lmask,
+                                                 a.lmask_g0, a.lmask_stride, tid, &stg);
         cy.have_prev = true;
         __syncthreads();
         for (uint32_t i = tid; i < tw; i += kThreads) {
