@@ -23,6 +23,14 @@ __global__ void __launch_bounds__(1024) k_red(uint32_t *out, int iters, int mode
             w[a] &= ~(1u << (i & 31));
             a = (a + 32 * p) & 8191;
         }
+    } else if (mode == 3) {
+        // 2 of 3 lanes active per RED (rotating): does the atomic unit cost scale with lanes?
+        const uint32_t pat = 0xB6DB6DB6u >> (lane % 3);     // 2 of every 3 bits set, lane-shifted
+        for (int i = 0; i < iters; ++i) {
+            if ((pat >> (i & 31)) & 1)
+                asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(base + 4 * a), "r"(~(1u << (i & 31))) : "memory");
+            a = (a + 32 * p) & 8191;
+        }
     } else {
         uint32_t x = tid, y = lane;
         for (int i = 0; i < iters; ++i) {
@@ -41,14 +49,15 @@ int main()
     uint32_t *d;
     cudaMalloc(&d, 8192);
     const int iters = 4096;
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 4; ++mode) {
         k_red<<<148, 1024>>>(d, iters, mode);
         if (cudaDeviceSynchronize() != cudaSuccess) { printf("kernel error\n"); return 1; }
         uint32_t c;
         cudaMemcpy(&c, d, 4, cudaMemcpyDeviceToHost);
         const double ops = 1024.0 * iters;
         printf("mode %d (%s): %u cycles, %.2f lane-ops/clk/SM\n", mode,
-               mode == 0 ? "red.shared.and" : mode == 1 ? "lds+and+sts" : "shf+lop3 x3", c, ops / c);
+               mode == 0 ? "red.shared.and" : mode == 1 ? "lds+and+sts" : mode == 2 ? "shf+lop3 x3" : "red, 2/3 lanes", c,
+               ops / c);
     }
     return 0;
 }
