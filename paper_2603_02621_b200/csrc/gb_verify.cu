@@ -756,12 +756,98 @@ __device__ __forceinline__ void block8q(LaneQ &m, uint32_t *h, int lane)
     hist8(c0, c1, c2, c3, c4, c5, c6, c7, h + J, lane);   // per warp and prime <= 32 kW 32 hits
 }
 
-template <int A, int J, bool DUMP, bool TRACK>
+template <int A, int J, int JEND, bool DUMP, bool TRACK>
 __device__ __forceinline__ void phase1q(LaneQ &m, uint32_t *h, int lane)
 {
-    if constexpr (J < kP1) {
+    if constexpr (J < JEND) {
         block8q<A, J, DUMP, TRACK>(m, h, lane);
-        phase1q<A, J + 8, DUMP, TRACK>(m, h, lane);
+        phase1q<A, J + 8, JEND, DUMP, TRACK>(m, h, lane);
+    }
+}
+
+// ---- phase 1b: the words still unresolved after candidate kC1, compacted to S
+// words per lane (a round's survivors gathered through the warp's queue area), so
+// candidates kC1 .. kP1-1 run only on live words.  Word k of a lane has its own
+// window position li[k].
+#ifndef GB_C1
+#define GB_C1 40
+#endif
+constexpr int kC1 = GB_C1;
+static_assert(kC1 % 8 == 0 && kC1 <= kP1, "compaction point on a block boundary");
+
+template <int S>
+struct LaneR {
+    const uint32_t *wa[S], *wb[S];  // class A / B window word aligned with U word k
+    uint32_t U[S];
+    uint32_t ws[S];
+    uint32_t lb[S], lu[S];
+    uint32_t li[S];                 // word index within the tile
+    uint32_t *dump[S];              // DUMP: dump entry of bit 0 of word k (bit b at +3b)
+};
+
+template <int A, int J, int S, bool DUMP>
+__device__ __forceinline__ uint32_t rstep(LaneR<S> &m, int k)
+{
+    constexpr uint32_t P = kTab[A / 2].p[J];
+    constexpr Trans T = trans(A, P);
+    constexpr int WA = (int)(T.shift >> 5);
+    constexpr uint32_t WB = T.shift & 31;
+    const uint32_t *src = T.src ? m.wb[k] : m.wa[k];
+    const uint32_t S_ = __funnelshift_l(src[-(WA + 1)], src[-WA], WB);
+    const uint32_t nw = m.U[k] & S_;
+    m.U[k] ^= nw;
+    const uint32_t c = __popc(nw);
+    m.ws[k] += c * P;
+    if constexpr (DUMP) {
+        uint32_t x = nw;
+        while (x) {
+            const int b = __ffs(x) - 1;
+            x &= x - 1;
+            m.dump[k][3 * b] = P;
+        }
+    }
+    return c;
+}
+
+template <int A, int J, int S, bool DUMP>
+__device__ __forceinline__ uint32_t rprime(LaneR<S> &m)
+{
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < S; ++k) c += rstep<A, J, S, DUMP>(m, k);
+    return c;
+}
+
+template <int A, int J, int S, bool DUMP, bool TRACK>
+__device__ __forceinline__ void block8r(LaneR<S> &m, uint32_t *h, int lane)
+{
+    uint32_t Ub[S];
+    if constexpr (TRACK) {
+#pragma unroll
+        for (int k = 0; k < S; ++k) Ub[k] = m.U[k];
+    }
+    const uint32_t c0 = rprime<A, J + 0, S, DUMP>(m);
+    const uint32_t c1 = rprime<A, J + 1, S, DUMP>(m);
+    const uint32_t c2 = rprime<A, J + 2, S, DUMP>(m);
+    const uint32_t c3 = rprime<A, J + 3, S, DUMP>(m);
+    const uint32_t c4 = rprime<A, J + 4, S, DUMP>(m);
+    const uint32_t c5 = rprime<A, J + 5, S, DUMP>(m);
+    const uint32_t c6 = rprime<A, J + 6, S, DUMP>(m);
+    const uint32_t c7 = rprime<A, J + 7, S, DUMP>(m);
+    if constexpr (TRACK) {
+#pragma unroll
+        for (int k = 0; k < S; ++k)
+            if (m.U[k] != Ub[k]) { m.lb[k] = J / 8 + 1; m.lu[k] = Ub[k]; }
+    }
+    hist8(c0, c1, c2, c3, c4, c5, c6, c7, h + J, lane);
+}
+
+template <int A, int J, int S, bool DUMP, bool TRACK>
+__device__ __forceinline__ void phase1r(LaneR<S> &m, uint32_t *h, int lane)
+{
+    if constexpr (J < kP1) {
+        block8r<A, J, S, DUMP, TRACK>(m, h, lane);
+        phase1r<A, J + 8, S, DUMP, TRACK>(m, h, lane);
     }
 }
 
@@ -834,6 +920,39 @@ __device__ __forceinline__ void replay_key_q(const LaneQ &m, uint64_t u0w, const
             if (nw) { lp = p; lbits = nw; }
         }
         const uint64_t n = 6 * ((u0w + 32 * k) * 32 + (uint64_t)(__ffs(lbits) - 1)) + A;
+        const uint64_t key = make_key(lp, n, a.origin);
+        if (key > acc.key) acc.key = key;
+    }
+}
+
+template <int A, int S>
+__device__ __forceinline__ void replay_key_r(const LaneR<S> &m, uint64_t u0, const VerifyArgs &a, uint32_t &best_p,
+                                             Acc &acc)
+{
+    uint32_t mx = 0;
+#pragma unroll
+    for (int k = 0; k < S; ++k) mx = max(mx, m.lb[k]);
+    const uint32_t bstar = __reduce_max_sync(FULL, mx);
+    if (bstar == 0) return;
+    const ClassTable &T = c_tab[A / 2];
+    if (T.p[8 * bstar - 1] < best_p) return;
+    const uint32_t jr = (bstar - 1) * 8;
+    best_p = max(best_p, T.p[jr]);
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+        if (m.lb[k] != bstar) continue;
+        uint32_t x = m.lu[k], lp = 0, lbits = 0;
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t p = T.p[jr + i];
+            const Trans t = trans(A, p);
+            const uint32_t *src = t.src ? m.wb[k] : m.wa[k];
+            const int wa = (int)(t.shift >> 5);
+            const uint32_t S_ = __funnelshift_l(src[-wa - 1], src[-wa], t.shift & 31);
+            const uint32_t nw = x & S_;
+            x ^= nw;
+            if (nw) { lp = p; lbits = nw; }
+        }
+        const uint64_t n = 6 * ((u0 + m.li[k]) * 32 + (uint64_t)(__ffs(lbits) - 1)) + A;
         const uint64_t key = make_key(lp, n, a.origin);
         if (key > acc.key) acc.key = key;
     }
@@ -1049,26 +1168,77 @@ struct ClassWork {
             m.ws[k] = 0;
             if (TRACK) { m.lb[k] = 0; m.lu[k] = 0; }
         }
-        phase1q<A, 0, DUMP, TRACK>(m, sh.histc[A / 2], lane);
+        phase1q<A, 0, kC1, DUMP, TRACK>(m, sh.histc[A / 2], lane);
 #pragma unroll
         for (int k = 0; k < kW; ++k) {
             acc.sum += m.ws[k];
             acc.chk += (uint64_t)m.ws[k] * (u0 + li0 + 32 * k);
         }
         if (TRACK) replay_key_q<A>(m, u0 + li0, a, best_p, acc);
-        // enqueue survivors
+        // survivors of candidates [0, kC1): staged past the queue's live entries,
+        // then compacted to 2 (or 1) words per lane for candidates [kC1, kP1)
+        uint32_t tot = 0;
 #pragma unroll
         for (int k = 0; k < kW; ++k) {
             const uint32_t bal = __ballot_sync(FULL, m.U[k] != 0);
             if (m.U[k]) {
-                const uint32_t pos = qn + __popc(bal & ((1u << lane) - 1));
+                const uint32_t pos = qn + tot + __popc(bal & ((1u << lane) - 1));
                 sh_qli(sh, warp)[pos] = (uint16_t)(li0 + 32 * k);
+                sh_qU(sh, warp)[pos] = m.U[k];
+            }
+            tot += __popc(bal);
+        }
+        __syncwarp();
+        const uint32_t q0 = qn;
+        for (uint32_t base = 0; base < tot; base += 64) {
+            const uint32_t cnt = min(64u, tot - base);
+            if (cnt > 32) stage<2, TRACK>(sh, qn, q0 + base, cnt, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+            else stage<1, TRACK>(sh, qn, q0 + base, cnt, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+        }
+        while (qn >= 32) batch(sh, qn, 32, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+    }
+
+    // candidates [kC1, kP1) for cnt staged words at queue entries e0.. (S per lane);
+    // survivors are appended to the queue (entries below e0 + 64 * pass: no overlap
+    // with staged words not yet read)
+    template <int S, bool TRACK>
+    static __device__ __forceinline__ void stage(Shared6 &sh, uint32_t &qn, uint32_t e0, uint32_t cnt, uint64_t u0,
+                                                 const uint32_t *wA, const uint32_t *wB, uint32_t halo,
+                                                 const VerifyArgs &a, Acc &acc, uint32_t &best_p, int lane, int warp)
+    {
+        LaneR<S> m;
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            const uint32_t idx = 32 * k + lane;
+            uint32_t li = 0, U = 0;
+            if (idx < cnt) { li = sh_qli(sh, warp)[e0 + idx]; U = sh_qU(sh, warp)[e0 + idx]; }
+            m.li[k] = li;
+            m.U[k] = U;
+            m.wa[k] = wA + halo + li;
+            m.wb[k] = wB + halo + li;
+            m.ws[k] = 0;
+            if (TRACK) { m.lb[k] = 0; m.lu[k] = 0; }
+            if (DUMP) m.dump[k] = a.dump + ((int64_t)(192 * (u0 + li) + A) - (int64_t)a.lo_e) / 2;
+        }
+        __syncwarp();                          // staged entries read before any append
+        phase1r<A, kC1, S, DUMP, TRACK>(m, sh.histc[A / 2], lane);
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            acc.sum += m.ws[k];
+            acc.chk += (uint64_t)m.ws[k] * (u0 + m.li[k]);
+        }
+        if (TRACK) replay_key_r<A, S>(m, u0, a, best_p, acc);
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            const uint32_t bal = __ballot_sync(FULL, m.U[k] != 0);
+            if (m.U[k]) {
+                const uint32_t pos = qn + __popc(bal & ((1u << lane) - 1));
+                sh_qli(sh, warp)[pos] = (uint16_t)m.li[k];
                 sh_qU(sh, warp)[pos] = m.U[k];
             }
             qn += __popc(bal);
         }
         __syncwarp();
-        while (qn >= 32) batch(sh, qn, 32, u0, wA, wB, halo, a, acc, best_p, lane, warp);
     }
 
     static __device__ __forceinline__ void round(Shared6 &sh, uint32_t &qn, uint32_t pair, uint32_t tw,
