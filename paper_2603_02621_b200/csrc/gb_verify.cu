@@ -185,6 +185,34 @@ __device__ __forceinline__ void mark_progression(uint32_t w, uint32_t off, uint3
     for (; i < n; ++i, ad += step) smem_and(ad, mask);
 }
 
+// both classes of one medium prime in one loop (their per-lane hit counts differ by
+// at most one): half the loop overhead per RED and two independent address streams
+__device__ __forceinline__ void mark_progression2(uint32_t wA, uint32_t offA, uint32_t hitsA, uint32_t wB,
+                                                  uint32_t offB, uint32_t hitsB, uint32_t p, uint32_t lane)
+{
+    const uint32_t nA = (hitsA + 31 - lane) >> 5, nB = (hitsB + 31 - lane) >> 5;
+    const uint32_t bA = offA + lane * p, bB = offB + lane * p;
+    const uint32_t mA = clear_mask(bA), mB = clear_mask(bB);
+    const uint32_t step = 4 * p;
+    uint32_t adA = wA + ((bA >> 5) << 2), adB = wB + ((bB >> 5) << 2);
+    const uint32_t n = min(nA, nB);
+    uint32_t i = 0;
+    for (; i + 2 <= n; i += 2, adA += 2 * step, adB += 2 * step) {
+        smem_and(adA, mA);
+        smem_and(adB, mB);
+        smem_and(adA + step, mA);
+        smem_and(adB + step, mB);
+    }
+    if (i < n) {
+        smem_and(adA, mA);
+        smem_and(adB, mB);
+        adA += step;
+        adB += step;
+    }
+    if (nA > n) smem_and(adA, mA);
+    if (nB > n) smem_and(adB, mB);
+}
+
 // Carried sieve offsets (per-CTA rows, ~92 MB at N = 1e12): L2 accesses with an
 // evict_last policy so the rows stay resident in L2 across tiles instead of making
 // a DRAM round trip per tile (GB_CARRY_NOHINT: plain .cg accesses, for A/B).
@@ -405,8 +433,12 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             const uint32_t pi = sp.i_med + rel;
             if (pi >= m_end) continue;
             const uint32_t p = __ldg(sp.primes + pi);
+#ifdef GB_MED_SPLIT
             mark_progression(sA, sh_mA[rel], p, sh_hA[rel], lane);
             mark_progression(sB, sh_mB[rel], p, sh_hB[rel], lane);
+#else
+            mark_progression2(sA, sh_mA[rel], sh_hA[rel], sB, sh_mB[rel], sh_hB[rel], p, lane);
+#endif
         }
     }
     // large primes: one thread per prime.  Steady primes: kB in flight per thread.
@@ -489,8 +521,20 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
 #pragma unroll
         for (int k = 0; k < kB; ++k) {
             const uint32_t p = pt[k].x, tm = pt[k].y;
+#ifdef GB_MULTI_SPLIT
             for (uint32_t b = oa[k]; b < nbits; b += p) clear_bit(sA, b);
             for (uint32_t b = ob[k]; b < nbits; b += p) clear_bit(sB, b);
+#else
+            {   // both classes in one loop (hit counts differ by at most one)
+                uint32_t ba = oa[k], bb = ob[k];
+                for (; ba < nbits && bb < nbits; ba += p, bb += p) {
+                    clear_bit(sA, ba);
+                    clear_bit(sB, bb);
+                }
+                for (; ba < nbits; ba += p) clear_bit(sA, ba);
+                for (; bb < nbits; bb += p) clear_bit(sB, bb);
+            }
+#endif
             const uint32_t pi = p0 + k * nt;
             if (pi < b2) {
                 carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
