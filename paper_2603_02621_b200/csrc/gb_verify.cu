@@ -185,6 +185,9 @@ __device__ __forceinline__ void mark_progression(uint32_t w, uint32_t off, uint3
     for (; i < n; ++i, ad += step) smem_and(ad, mask);
 }
 
+#ifndef GB_MP2_UNROLL
+#define GB_MP2_UNROLL 2
+#endif
 // both classes of one medium prime in one loop (their per-lane hit counts differ by
 // at most one): half the loop overhead per RED and two independent address streams
 __device__ __forceinline__ void mark_progression2(uint32_t wA, uint32_t offA, uint32_t hitsA, uint32_t wB,
@@ -197,17 +200,29 @@ __device__ __forceinline__ void mark_progression2(uint32_t wA, uint32_t offA, ui
     uint32_t adA = wA + ((bA >> 5) << 2), adB = wB + ((bB >> 5) << 2);
     const uint32_t n = min(nA, nB);
     uint32_t i = 0;
+#if GB_MP2_UNROLL >= 4
+    for (; i + 4 <= n; i += 4, adA += 4 * step, adB += 4 * step) {
+        smem_and(adA, mA);
+        smem_and(adB, mB);
+        smem_and(adA + step, mA);
+        smem_and(adB + step, mB);
+        smem_and(adA + 2 * step, mA);
+        smem_and(adB + 2 * step, mB);
+        smem_and(adA + 3 * step, mA);
+        smem_and(adB + 3 * step, mB);
+    }
+#endif
+#if GB_MP2_UNROLL >= 2
     for (; i + 2 <= n; i += 2, adA += 2 * step, adB += 2 * step) {
         smem_and(adA, mA);
         smem_and(adB, mB);
         smem_and(adA + step, mA);
         smem_and(adB + step, mB);
     }
-    if (i < n) {
+#endif
+    for (; i < n; ++i, adA += step, adB += step) {
         smem_and(adA, mA);
         smem_and(adB, mB);
-        adA += step;
-        adB += step;
     }
     if (nA > n) smem_and(adA, mA);
     if (nB > n) smem_and(adB, mB);
@@ -527,6 +542,14 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
 #else
             {   // both classes in one loop (hit counts differ by at most one)
                 uint32_t ba = oa[k], bb = ob[k];
+#ifndef GB_MH_NOUNROLL
+                for (; ba + p < nbits && bb + p < nbits; ba += 2 * p, bb += 2 * p) {   // 2 hits per class
+                    clear_bit(sA, ba);
+                    clear_bit(sB, bb);
+                    clear_bit(sA, ba + p);
+                    clear_bit(sB, bb + p);
+                }
+#endif
                 for (; ba < nbits && bb < nbits; ba += p, bb += p) {
                     clear_bit(sA, ba);
                     clear_bit(sB, bb);
