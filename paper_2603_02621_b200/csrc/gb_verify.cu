@@ -163,33 +163,14 @@ __device__ __forceinline__ void clear_bit(uint32_t w, uint32_t b)
     smem_and(w + ((b >> 5) << 2), clear_mask(b));
 }
 
-__device__ __forceinline__ void mark_progression(uint32_t w, uint32_t off, uint32_t p, uint32_t hits,
-                                                 uint32_t lane)
-{
-    // one warp, one prime: lane l marks hits l, l + 32, ... (bits off + (l + 32i) p).
-    // The stride is p whole words, so a lane's bit-in-word (hence its mask) never
-    // changes: only the word address moves, by 4p bytes per hit.
-    const uint32_t n = (hits + 31 - lane) >> 5;         // this lane's hit count
-    if (n == 0) return;
-    const uint32_t b0 = off + lane * p;
-    const uint32_t mask = clear_mask(b0);
-    const uint32_t step = 4 * p;
-    uint32_t ad = w + ((b0 >> 5) << 2);
-    uint32_t i = 0;
-    for (; i + 4 <= n; i += 4, ad += 4 * step) {
-        smem_and(ad, mask);
-        smem_and(ad + step, mask);
-        smem_and(ad + 2 * step, mask);
-        smem_and(ad + 3 * step, mask);
-    }
-    for (; i < n; ++i, ad += step) smem_and(ad, mask);
-}
-
 #ifndef GB_MP2_UNROLL
 #define GB_MP2_UNROLL 2
 #endif
-// both classes of one medium prime in one loop (their per-lane hit counts differ by
-// at most one): half the loop overhead per RED and two independent address streams
+// One warp, one medium prime, both classes: lane l marks hits l, l + 32, ... of each
+// class (bits off + (l + 32i) p).  The stride is p whole words, so a lane's bit-in-
+// word (hence its mask) never changes: only the word address moves, by 4p bytes per
+// hit.  The two classes' per-lane hit counts differ by at most one, so they share one
+// loop (half the loop overhead per RED, two independent address streams).
 __device__ __forceinline__ void mark_progression2(uint32_t wA, uint32_t offA, uint32_t hitsA, uint32_t wB,
                                                   uint32_t offB, uint32_t hitsB, uint32_t p, uint32_t lane)
 {
@@ -448,12 +429,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             const uint32_t pi = sp.i_med + rel;
             if (pi >= m_end) continue;
             const uint32_t p = __ldg(sp.primes + pi);
-#ifdef GB_MED_SPLIT
-            mark_progression(sA, sh_mA[rel], p, sh_hA[rel], lane);
-            mark_progression(sB, sh_mB[rel], p, sh_hB[rel], lane);
-#else
             mark_progression2(sA, sh_mA[rel], sh_hA[rel], sB, sh_mB[rel], sh_hB[rel], p, lane);
-#endif
         }
     }
     // large primes: one thread per prime.  Steady primes: kB in flight per thread.
