@@ -1201,15 +1201,34 @@ struct ClassWork {
         m.wa = wA + halo + li0;           // words past tw read window slack; their U is 0
         m.wb = wB + halo + li0;
         m.dump0 = DUMP ? a.dump + ((int64_t)(192 * (u0 + li0) + A) - (int64_t)a.lo_e) / 2 : nullptr;
+        // warp-uniform: every word of the round inside the tile and the class's m range
+        // (and not the word holding n = 4 and 6) -> all 32 evens of each word are live
+        const uint64_t ub = u0 + pair * 32 * kW;
+        const bool interior = pair * 32 * kW + 32 * kW <= tw && ub != 0 && ub * 32 >= a.m_lo[A / 2] &&
+                              (ub + 32 * kW) * 32 <= a.m_hi[A / 2];
+#ifdef GB_NO_INTERIOR
+        if (false) {
+#else
+        if (interior) {
+#endif
 #pragma unroll
-        for (int k = 0; k < kW; ++k) {
-            const uint32_t li = li0 + 32 * k;
-            uint32_t U = li < tw ? valid_mask<A>(u0 + li, a) : 0u;
-            acc.evens += __popc(U);
-            if (k == 0) U = take_special<A, DUMP>(U, u0 + li, sh.hist, a, acc);
-            m.U[k] = U;
-            m.ws[k] = 0;
-            if (TRACK) { m.lb[k] = 0; m.lu[k] = 0; }
+            for (int k = 0; k < kW; ++k) {
+                m.U[k] = FULL;
+                m.ws[k] = 0;
+                if (TRACK) { m.lb[k] = 0; m.lu[k] = 0; }
+            }
+            acc.evens += 32 * kW;
+        } else {
+#pragma unroll
+            for (int k = 0; k < kW; ++k) {
+                const uint32_t li = li0 + 32 * k;
+                uint32_t U = li < tw ? valid_mask<A>(u0 + li, a) : 0u;
+                acc.evens += __popc(U);
+                if (k == 0) U = take_special<A, DUMP>(U, u0 + li, sh.hist, a, acc);
+                m.U[k] = U;
+                m.ws[k] = 0;
+                if (TRACK) { m.lb[k] = 0; m.lu[k] = 0; }
+            }
         }
         phase1q<A, 0, kC1, DUMP, TRACK>(m, sh.histc[A / 2], lane);
 #pragma unroll
@@ -1338,7 +1357,7 @@ __device__ __forceinline__ void mark_tile(Shared6 &sh, uint32_t &next_round, uin
         if (lane == 0) r = atomicAdd(&next_round, 1u);
         r = __shfl_sync(FULL, r, 0);
         if (r >= 3 * r1) break;
-        const int cls = (int)(r / r1);
+        const int cls = r >= r1 ? (r >= 2 * r1 ? 2 : 1) : 0;      // no integer division
         const uint32_t pair = r - (uint32_t)cls * r1;
         if (cls != qcls) {
             flush_queue<DUMP, UNROLL>(qcls, sh, qn, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
