@@ -238,6 +238,10 @@ def main():
     if world > 1:
         dist.barrier()
     launches = gb.gb_launch_count() - launches0
+    if world > 1:                                    # whole job: every rank's launches
+        lt = torch.tensor([launches], dtype=torch.int64, device=dev)
+        dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+        launches = int(lt[0])
     clocks = sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b, _ in results]
     kern_ms = [a.elapsed_time(b) for a, b in k_events]
