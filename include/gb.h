@@ -169,7 +169,8 @@ gb_status gb_verify_range_host(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p
  * scratch (segments of 2^28 evens); otherwise deterministic MR64
  * (PAPER.md:89).  Unresolved n go to the same exhaustive fallback.  Same
  * arguments, result semantics and errors as gb_verify_range, and results identical
- * to it field by field; two launches per segment.  Not the product path: it
+ * to it field by field; per segment one sieve launch (plus K-LARGE mask launches
+ * above 2^21) and one per-n launch.  Not the product path: it
  * exists to measure per-n lookups against the inverted bulk marking on one box. */
 gb_status gb_verify_range_pern(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_max,
                                int64_t *d_result, uint32_t *d_pmin_dump, void *stream);
