@@ -108,6 +108,38 @@ struct Acc {
     uint64_t key = 0, first_unres = UINT64_MAX;
 };
 
+// End of a kernel: warp-reduce a thread's accumulators, then one atomic per warp per
+// result field (SUM / MAX / MIN as include/gb.h defines them).
+__device__ __forceinline__ void flush_acc(const Acc &acc, int64_t *result, int lane)
+{
+    auto wsum = [](uint64_t v) {
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        return v;
+    };
+    auto wmax = [](uint64_t v) {
+        for (int o = 16; o; o >>= 1) { const uint64_t w = __shfl_xor_sync(FULL, v, o); v = w > v ? w : v; }
+        return v;
+    };
+    auto wmin = [](uint64_t v) {
+        for (int o = 16; o; o >>= 1) { const uint64_t w = __shfl_xor_sync(FULL, v, o); v = w < v ? w : v; }
+        return v;
+    };
+    const uint64_t ev = wsum(acc.evens), vf = wsum(acc.verified), fu = wsum(acc.fast_unres);
+    const uint64_t un = wsum(acc.unres), sm = wsum(acc.sum), ck = wsum(acc.chk);
+    const uint64_t ky = wmax(acc.key), fr = wmin(acc.first_unres);
+    unsigned long long *R = (unsigned long long *)result;
+    if (lane == 0) {
+        if (ev) atomicAdd(R + GB_R_EVENS, ev);
+        if (vf) atomicAdd(R + GB_R_VERIFIED, vf);
+        if (fu) atomicAdd(R + GB_R_FASTPATH_UNRESOLVED, fu);
+        if (un) atomicAdd(R + GB_R_UNRESOLVED, un);
+        if (sm) atomicAdd(R + GB_R_SUM_PMIN, sm);
+        if (ck) atomicAdd(R + GB_R_CHK_RAW, ck);
+        if (ky) atomicMax(R + GB_R_MAX_KEY, ky);
+        if (fr != UINT64_MAX) atomicMin(R + GB_R_FIRST_UNRESOLVED_N, fr);
+    }
+}
+
 // GB_R_MAX_KEY encoding: largest p first, then the smallest n
 __device__ __forceinline__ uint64_t make_key(uint64_t p, uint64_t n, uint64_t origin)
 {

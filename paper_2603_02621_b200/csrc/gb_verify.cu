@@ -1501,33 +1501,7 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(GB_PARAM)
 #endif
     acc.verified = acc.evens - acc.unres;
 
-    // flush: warp-reduce then one atomic per warp per field
-    auto wsum = [&](uint64_t v) {
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-        return v;
-    };
-    auto wmax = [&](uint64_t v) {
-        for (int o = 16; o; o >>= 1) { uint64_t w = __shfl_xor_sync(FULL, v, o); v = w > v ? w : v; }
-        return v;
-    };
-    auto wmin = [&](uint64_t v) {
-        for (int o = 16; o; o >>= 1) { uint64_t w = __shfl_xor_sync(FULL, v, o); v = w < v ? w : v; }
-        return v;
-    };
-    const uint64_t ev = wsum(acc.evens), vf = wsum(acc.verified), fu = wsum(acc.fast_unres);
-    const uint64_t un = wsum(acc.unres), sm = wsum(acc.sum), ck = wsum(acc.chk);
-    const uint64_t ky = wmax(acc.key), fr = wmin(acc.first_unres);
-    unsigned long long *R = (unsigned long long *)a.result;
-    if (lane == 0) {
-        if (ev) atomicAdd(R + GB_R_EVENS, ev);
-        if (vf) atomicAdd(R + GB_R_VERIFIED, vf);
-        if (fu) atomicAdd(R + GB_R_FASTPATH_UNRESOLVED, fu);
-        if (un) atomicAdd(R + GB_R_UNRESOLVED, un);
-        if (sm) atomicAdd(R + GB_R_SUM_PMIN, sm);
-        if (ck) atomicAdd(R + GB_R_CHK_RAW, ck);
-        if (ky) atomicMax(R + GB_R_MAX_KEY, ky);
-        if (fr != UINT64_MAX) atomicMin(R + GB_R_FIRST_UNRESOLVED_N, fr);
-    }
+    flush_acc(acc, a.result, lane);
 }
 
 
