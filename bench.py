@@ -46,12 +46,17 @@ def parse():
                     help="bulk: the product path (inverted bulk marking); pern: the paper's per-n "
                          "gpu3 kernel (NEXT-1, PAPER.md:82-95); resident: the paper's gpu2 with the "
                          "whole odd bitset of [3, hi) sieved into HBM each step (NEXT-2, PAPER.md:41-59)")
-    ap.add_argument("--strips-per-rank", type=int, default=8)
+    ap.add_argument("--strips-per-rank", type=int, default=None,
+                    help="default 8 for c4 (balances the growth of work with n), 2 for c5 (the "
+                         "window's cost is flat; fewer partial K-LARGE chunks)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sieve", action="store_true", help="skip the standalone sieve GB/s leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.strips_per_rank is None:
+        a.strips_per_rank = 2 if a.workload == "c5" else 8
+    return a
 
 
 # ----------------------------------------------------------------- clocks
