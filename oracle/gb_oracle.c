@@ -35,9 +35,14 @@
  *   R5 aggregates: histogram of p_min by prime index (bin 0 = unresolved,
  *      bin i = i-th prime, p_1 = 2, ..., p_6542 = 65521, bin 6543 = larger),
  *      max p_min with the SMALLEST n attaining it (A025018 convention),
- *      sum of p_min, and chk = sum of p_min(n) * floor(n / 192) mod 2^64
- *      (reading R6: a checksum sensitive to which 192-integer block
- *      each p_min lands in; the paper defines none).
+ *      sum of p_min, and two checksums (the paper defines none; R6):
+ *        chk    = sum of n * p_min(n) mod 2^64 (a
+ *                 p_min placed on the wrong n changes it);
+ *        chk192 = sum of p_min(n) * floor(n / 192) mod 2^64 (coarser: which
+ *                 192-integer block each p_min lands in; a second plain
+ *                 function of the per-n values, compared where no dump is);
+ *      optionally chk per chunk of 2^k evens counted from lo_e (chunk_chk),
+ *      so full-range goldens can be compared piece by piece.
  *
  * Build: gcc -O2 -std=c11 -pthread -shared -fPIC gb_oracle.c -o liboracle.so
  */
@@ -60,7 +65,8 @@ typedef struct {
     int64_t max_pmin;            /* 0 if no verified n */
     int64_t max_pmin_n;          /* smallest n with p_min == max_pmin */
     int64_t sum_pmin;
-    uint64_t chk;                /* sum p_min(n) * floor(n/192)  mod 2^64 */
+    uint64_t chk;                /* sum n * p_min(n)             mod 2^64 */
+    uint64_t chk192;             /* sum p_min(n) * floor(n/192)  mod 2^64 */
     int64_t hist[OR_NBINS];
 } or_result;
 
@@ -170,6 +176,9 @@ typedef struct {
     uint64_t p_fast, cap;
     int tid, nthreads;
     uint32_t *dump;             /* may be NULL; index (n - lo_e)/2 */
+    uint64_t *chunk_chk;        /* may be NULL; chk per chunk_evens evens from lo_e */
+    uint64_t chunk_evens;
+    uint64_t seg_chk;           /* chk of the current segment */
     or_result res;
     int err;
 } worker;
@@ -204,7 +213,9 @@ static void record(worker *w, uint64_t n, uint64_t p)
     if (p > w->p_fast) r->fastpath_unresolved++;
     r->hist[bin_of(w->sp, p)]++;
     r->sum_pmin += (int64_t)p;
-    r->chk += (uint64_t)p * (n / 192);
+    r->chk += n * p;                           /* wraps mod 2^64 */
+    r->chk192 += p * (n / 192);
+    w->seg_chk += n * p;
     if ((int64_t)p > r->max_pmin || ((int64_t)p == r->max_pmin && (int64_t)n < r->max_pmin_n)) {
         r->max_pmin = (int64_t)p;
         r->max_pmin_n = (int64_t)n;
@@ -226,6 +237,7 @@ static void *worker_main(void *arg)
         uint64_t wlo = (n0 > 3 + OR_WINDOW_BELOW) ? n0 - OR_WINDOW_BELOW : 3;
         if (wlo % 2 == 0) wlo -= 1;
         sieve_odd_window(sp, wlo, n1, comp);
+        w->seg_chk = 0;
         for (uint64_t n = n0; n < n1; n += 2) {
             uint64_t found = 0;
             if (n == 4) {
@@ -247,6 +259,9 @@ static void *worker_main(void *arg)
             }
             record(w, n, found);
         }
+        if (w->chunk_chk)                           /* a segment lies inside one chunk */
+            __atomic_fetch_add(&w->chunk_chk[(n0 - w->lo_e) / 2 / w->chunk_evens], w->seg_chk,
+                               __ATOMIC_RELAXED);
     }
     free(comp);
     return NULL;
@@ -265,6 +280,7 @@ static void merge(or_result *a, const or_result *b)
     }
     a->sum_pmin += b->sum_pmin;
     a->chk += b->chk;
+    a->chk192 += b->chk192;
     for (int i = 0; i < OR_NBINS; i++) a->hist[i] += b->hist[i];
 }
 
@@ -276,16 +292,24 @@ static void merge(or_result *a, const or_result *b)
  *   out      : aggregates (R5)
  *   dump     : optional u32 per even n, index (n - lo_e)/2, lo_e = max(4, lo
  *              rounded up to even); value p_min, 0 = unresolved.
+ *   chunk_chk: optional; chunk_chk[c] = chk over the evens with index (n - lo_e)/2
+ *              in [c * chunk_evens, (c + 1) * chunk_evens); the caller zeroes
+ *              ceil(evens / chunk_evens) entries.  chunk_evens: a power of two.
  * Returns 0 on success, -1 on allocation failure, -2 on bad arguments.
  */
 int or_verify(uint64_t lo, uint64_t hi, uint64_t p_fast, uint64_t cap, int threads,
-              or_result *out, uint32_t *dump)
+              or_result *out, uint32_t *dump, uint64_t *chunk_chk, uint64_t chunk_evens)
 {
     result_clear(out);
     if (threads < 1) threads = 1;
     uint64_t lo_e = lo < 4 ? 4 : lo + (lo & 1);
     if (hi <= lo_e) return 0;                               /* empty range */
     if (hi > (1ull << 62)) return -2;
+    uint64_t seg_evens = 1u << 22;
+    if (chunk_chk) {
+        if (chunk_evens == 0 || (chunk_evens & (chunk_evens - 1))) return -2;
+        if (chunk_evens < seg_evens) seg_evens = chunk_evens;   /* segments nest in chunks */
+    }
     small_primes sp;
     if (small_primes_make(&sp, or_isqrt(hi - 1) + 1) != 0) return -1;
     worker *ws = (worker *)calloc((size_t)threads, sizeof(worker));
@@ -293,9 +317,10 @@ int or_verify(uint64_t lo, uint64_t hi, uint64_t p_fast, uint64_t cap, int threa
     if (!ws || !th) { small_primes_free(&sp); free(ws); free(th); return -1; }
     for (int t = 0; t < threads; t++) {
         ws[t].sp = &sp; ws[t].lo_e = lo_e; ws[t].hi = hi;
-        ws[t].seg_evens = 1u << 22;
+        ws[t].seg_evens = seg_evens;
         ws[t].p_fast = p_fast; ws[t].cap = cap;
         ws[t].tid = t; ws[t].nthreads = threads; ws[t].dump = dump;
+        ws[t].chunk_chk = chunk_chk; ws[t].chunk_evens = chunk_evens;
         result_clear(&ws[t].res);
         pthread_create(&th[t], NULL, worker_main, &ws[t]);
     }

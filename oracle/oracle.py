@@ -19,7 +19,10 @@ LIB = os.path.join(HERE, "liboracle.so")
 NBINS = 6544
 U64_MAX = (1 << 64) - 1
 FIELDS = ("evens", "verified", "fastpath_unresolved", "unresolved",
-          "first_unresolved_n", "max_pmin", "max_pmin_n", "sum_pmin", "chk")
+          "first_unresolved_n", "max_pmin", "max_pmin_n", "sum_pmin", "chk", "chk192")
+# the aggregates libgb's result vector carries (chk = sum n*p_min needs the per-n
+# values: tests compare it through dumps, see chk_of_dump)
+AGG_FIELDS = tuple(f for f in FIELDS if f != "chk")
 
 
 class OrResult(ctypes.Structure):
@@ -27,7 +30,8 @@ class OrResult(ctypes.Structure):
                 ("fastpath_unresolved", ctypes.c_int64), ("unresolved", ctypes.c_int64),
                 ("first_unresolved_n", ctypes.c_int64), ("max_pmin", ctypes.c_int64),
                 ("max_pmin_n", ctypes.c_int64), ("sum_pmin", ctypes.c_int64),
-                ("chk", ctypes.c_uint64), ("hist", ctypes.c_int64 * NBINS)]
+                ("chk", ctypes.c_uint64), ("chk192", ctypes.c_uint64),
+                ("hist", ctypes.c_int64 * NBINS)]
 
 
 def build(force: bool = False) -> str:
@@ -55,7 +59,7 @@ def lib():
         L.or_verify.restype = ctypes.c_int
         L.or_verify.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                 ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(OrResult),
-                                ctypes.c_void_p]
+                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64]
         L.or_sieve_window.restype = ctypes.c_int
         L.or_sieve_window.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p]
         L.or_prime_pi.restype = ctypes.c_uint64
@@ -104,14 +108,23 @@ def n_evens(lo: int, hi: int) -> int:
 
 
 def verify(lo: int, hi: int, p_fast: int = 65521, cap: int = U64_MAX,
-           threads: int | None = None, dump: bool = False):
-    """Aggregates (dict with FIELDS + 'hist') and optional per-n u32 dump."""
+           threads: int | None = None, dump: bool = False, chunk_evens: int | None = None):
+    """Aggregates (dict with FIELDS + 'hist') and optional per-n u32 dump.
+    chunk_evens (a power of two): also out['chunk_chk'], a uint64 array with the
+    chk (sum n * p_min mod 2^64) of each chunk of that many evens from lo_e."""
     res = OrResult()
-    d = np.zeros(n_evens(lo, hi), dtype=np.uint32) if dump else None
+    ne = n_evens(lo, hi)
+    d = np.zeros(ne, dtype=np.uint32) if dump else None
+    ch = None
+    if chunk_evens:
+        ch = np.zeros(max(1, -(-ne // chunk_evens)), dtype=np.uint64)
     rc = lib().or_verify(lo, hi, p_fast, cap, threads or default_threads(), ctypes.byref(res),
-                         d.ctypes.data if (d is not None and d.size) else None)
+                         d.ctypes.data if (d is not None and d.size) else None,
+                         ch.ctypes.data if ch is not None else None, chunk_evens or 0)
     if rc != 0:
         raise RuntimeError(f"or_verify rc={rc}")
     out = {f: int(getattr(res, f)) for f in FIELDS}
     out["hist"] = np.ctypeslib.as_array(res.hist).copy()
+    if ch is not None:
+        out["chunk_chk"] = ch
     return out, d

@@ -44,7 +44,7 @@ def main():
     ap.add_argument("--threads", type=int, default=oracle.default_threads())
     a = ap.parse_args()
     out = {"source": "oracle/gb_oracle.c via scripts/make_golden_4e18.py (CPU oracle only)",
-           "p_fast": 65521, "chk_def": "sum p_min(n)*floor(n/192) mod 2^64 (DESIGN.md R6)",
+           "p_fast": 65521, "chk_def": "chk = sum n*p_min(n) mod 2^64 (SURVEY.md 8(b)); chk192 = sum p_min(n)*floor(n/192) mod 2^64",
            "dump_hash": "sha256 of the u32 little-endian per-n dump", "windows": []}
     for lo, hi in windows(a.evens):
         t0 = time.time()

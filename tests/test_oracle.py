@@ -116,7 +116,8 @@ def test_brute_force_small():
     assert r["evens"] == len(want) and r["unresolved"] == 0
     assert r["sum_pmin"] == int(want.sum())
     ns = np.arange(4, hi, 2, dtype=np.uint64)
-    assert r["chk"] == int((want.astype(np.uint64) * (ns // 192)).sum()) & U64
+    assert r["chk"] == int((want.astype(np.uint64) * ns).sum()) & U64
+    assert r["chk192"] == int((want.astype(np.uint64) * (ns // 192)).sum()) & U64
     idx = prime_index_bins()
     h = np.zeros(oracle.NBINS, dtype=np.int64)
     for p in want:
@@ -176,10 +177,27 @@ def test_closed_form_bins(N):
 
 
 def test_sum_n_pmin_1e6():
-    # sum n * p_min over [4, 1e6] = 5,216,083,445,938
+    # SURVEY.md Appendix A (an independent brute-force program): sum n * p_min over
+    # [4, 1e6] = 5,216,083,445,938 -- the oracle's chk (SURVEY 8(b) definition; no
+    # wrap below 2^64 here), and the same from its dump
     r, d = oracle.verify(4, 10**6 + 1, dump=True)
     ns = np.arange(4, 10**6 + 1, 2, dtype=np.int64)
     assert int((ns * d.astype(np.int64)).sum()) == AGG["1000000"]["sum_n_pmin"]
+    assert r["chk"] == AGG["1000000"]["sum_n_pmin"]
+
+
+def test_chunk_checksums():
+    """Per-chunk chk (the golden format of scripts/make_golden.py): each chunk's
+    value is sum n * p_min over its evens (from the dump, numpy uint64 wrap), for a
+    range with a ragged last chunk and an odd lo, and for chunks smaller than the
+    oracle's segments."""
+    for lo, hi, ce in ((4, 300001, 1 << 14), (1001, 2 * 10**6 + 7, 1 << 16), (10**12 - 10**6 + 1, 10**12, 1 << 17)):
+        r, d = oracle.verify(lo, hi, dump=True, chunk_evens=ce)
+        ns = oracle.lo_even(lo) + 2 * np.arange(d.size, dtype=np.uint64)
+        prod = ns * d.astype(np.uint64)
+        want = [int(prod[i:i + ce].sum()) & U64 for i in range(0, d.size, ce)]
+        assert [int(x) for x in r["chunk_chk"]] == want
+        assert sum(want) & U64 == r["chk"]
 
 
 def test_additivity_and_edges():
@@ -194,10 +212,11 @@ def test_additivity_and_edges():
         for k in ("evens", "verified", "fastpath_unresolved", "unresolved", "sum_pmin"):
             acc[k] += r[k]
         acc["chk"] = (acc["chk"] + r["chk"]) & U64
+        acc["chk192"] = (acc["chk192"] + r["chk192"]) & U64
         acc["hist"] = acc["hist"] + r["hist"]
         if (r["max_pmin"], -r["max_pmin_n"]) > (acc["max_pmin"], -acc["max_pmin_n"]):
             acc["max_pmin"], acc["max_pmin_n"] = r["max_pmin"], r["max_pmin_n"]
-    for k in ("evens", "verified", "sum_pmin", "chk", "max_pmin", "max_pmin_n"):
+    for k in ("evens", "verified", "sum_pmin", "chk", "chk192", "max_pmin", "max_pmin_n"):
         assert acc[k] == full[k], k
     assert np.array_equal(acc["hist"], full["hist"])
     # empty / degenerate ranges
