@@ -50,7 +50,7 @@ typedef struct gb_ctx gb_ctx;   /* opaque; host object owned by libgb */
  * FIRST_UNRESOLVED_N (MIN) and MAX_KEY (MAX) -- the reduction rules the
  * multi-GPU layer applies with NCCL ("--gpus distributes work").
  * ------------------------------------------------------------------------- */
-#define GB_RESULT_VERSION 0x4742000000000001LL
+#define GB_RESULT_VERSION 0x4742000000000002LL
 #define GB_R_VERSION              0   /* GB_RESULT_VERSION                           */
 #define GB_R_EVENS                1   /* SUM: even n in the verified ranges          */
 #define GB_R_VERIFIED             2   /* SUM: n with a partition found               */
@@ -59,20 +59,29 @@ typedef struct gb_ctx gb_ctx;   /* opaque; host object owned by libgb */
 #define GB_R_UNRESOLVED           4   /* SUM: n with no partition p <= n/2 (a
                                          counterexample) -- must be 0                */
 #define GB_R_SUM_PMIN             5   /* SUM: sum of p_min                           */
-#define GB_R_CHK_LO32             6   /* SUM: low 32 bits of CHK (after finalize)    */
-#define GB_R_CHK_HI32             7   /* SUM: high 32 bits of CHK (after finalize)   */
+#define GB_R_CHK_LO32             6   /* SUM: low 32 bits of CHK192 (after finalize) */
+#define GB_R_CHK_HI32             7   /* SUM: high 32 bits of CHK192 (after finalize)*/
 #define GB_R_FIRST_UNRESOLVED_N   8   /* MIN: smallest unresolved n, INT64_MAX if none */
-#define GB_R_MAX_KEY              9   /* MAX: (p_min << 40) | (2^40-1 - (n-origin)/2);
-                                         largest p_min, ties to the smallest n       */
-#define GB_R_CHK_RAW             10   /* device accumulator of CHK = sum of
-                                         p_min(n) * floor(n/192) mod 2^64; moved
-                                         into LO32/HI32 and zeroed by finalize       */
+#define GB_R_MAX_KEY              9   /* MAX: (min(p_min, 2^14-1) << 49) |
+                                         (2^49-1 - (n-origin)/2): largest p_min, ties
+                                         to the smallest n (exact while p_min < 2^14;
+                                         every p_min below 4e18 is <= 9781)          */
+#define GB_R_CHK_RAW             10   /* device accumulator of CHK192 = sum of
+                                         p_min(n) * floor(n/192) mod 2^64 (a block
+                                         checksum: which 192-integer block each
+                                         p_min lands in); moved into LO32/HI32 and
+                                         zeroed by finalize.  The exact sum of
+                                         n * p_min needs the per-n values: see the
+                                         dump of gb_verify_range                    */
+#define GB_R_MAX_PMIN_RAW        11   /* MAX: largest p_min (exact even when the
+                                         MAX_KEY field saturates at 2^14-1)         */
 #define GB_R_HIST                16   /* SUM: hist[0..GB_NBINS)                       */
 #define GB_NBINS               6544   /* hist[0] = unresolved; hist[i] = #n with p_min
                                          = i-th prime (p_1 = 2, p_2 = 3, ...,
                                          p_6542 = 65521); hist[6543] = p_min > 65521 */
 #define GB_RESULT_WORDS (GB_R_HIST + GB_NBINS)
-#define GB_KEY_SHIFT 40
+#define GB_KEY_SHIFT 49
+#define GB_KEY_PMAX 16383              /* 2^14 - 1: p field of MAX_KEY (saturating) */
 
 /* Largest p_max accepted (the fast-path prime bound, PAPER.md:173 P_SMALL = 1e6). */
 #define GB_PMAX_LIMIT 1048576u
@@ -91,7 +100,7 @@ size_t gb_ctx_workspace_bytes(uint64_t hi_max, uint32_t p_max);
  * of all primes <= R = max(isqrt(hi_max - 1), p_max), as an odd-only bitset
  * plus an ascending u32 list, built on the GPU inside d_workspace.
  *   origin  : even n origin for GB_R_MAX_KEY; every verified n must satisfy
- *             origin <= n and (n - origin)/2 < 2^40.
+ *             origin <= n and (n - origin)/2 < 2^49 (one result spans 1.1e15).
  *   hi_max  : exclusive upper bound of every later range.
  *   p_max   : largest fast-path bound later calls may use (3..GB_PMAX_LIMIT).
  * Synchronizes `stream`.  On error *out is NULL. */
@@ -121,7 +130,8 @@ gb_status gb_sieve_segment(gb_ctx *ctx, uint64_t word_lo, uint64_t n_words,
                            uint64_t *d_words, void *stream);
 
 /* Set d_result (GB_RESULT_WORDS int64) to its initial state on the stream:
- * version word, counters 0, FIRST_UNRESOLVED_N = INT64_MAX, MAX_KEY = 0. */
+ * version word, counters 0, FIRST_UNRESOLVED_N = INT64_MAX, MAX_KEY = 0.  Runs
+ * on the device that owns d_result. */
 gb_status gb_result_init(int64_t *d_result, void *stream);
 
 /* After a rank's last gb_verify_range: move CHK_RAW into CHK_LO32/CHK_HI32 (so
@@ -142,7 +152,7 @@ gb_status gb_result_finalize(int64_t *d_result, void *stream);
  * chunks of whole tiles, each a K-LARGE mask fill + marking launch and a verify
  * launch.
  * Errors: GB_EINVAL (p_max < 3 or > the ctx's p_max, hi > GB_HI_LIMIT,
- * n < origin, (hi - origin)/2 >= 2^40, misaligned pointers), GB_ERANGE
+ * n < origin, (hi - origin)/2 >= 2^49, misaligned pointers), GB_ERANGE
  * (hi > ctx hi_max). */
 gb_status gb_verify_range(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_max,
                           int64_t *d_result, uint32_t *d_pmin_dump, void *stream);

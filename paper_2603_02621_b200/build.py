@@ -44,8 +44,7 @@ def build(force: bool = False, verbose: bool = False, defines: list[str] | None 
         return LIB
     objs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        obj = obj.replace(".o", f".{os.getpid()}.o")
+        obj = os.path.join(CSRC, f"{os.path.splitext(src)[0]}.{os.getpid()}.o")
         cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in (defines or [])], "-I", INCLUDE, "-I", CSRC,
                "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)

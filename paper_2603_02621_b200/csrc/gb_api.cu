@@ -94,19 +94,17 @@ uint32_t count_le(const std::vector<uint32_t> &v, uint64_t x)
 
 // wheel halo: the largest shift of a candidate p is p/6 + 1 bits
 uint32_t verify_halo(uint32_t p_top) { return ((p_top / 6 + 1) >> 5) + 1; }
-// the two class windows must fit next to the kernel's static shared memory
-constexpr uint32_t kVerifyDynSmemMax = 168 * 1024;   // the two windows; + queues + static <= 227 KB
-constexpr uint32_t kWinSlackWords = 128;   // = kWinSlack in gb_verify.cu
+// the two class windows must fit next to the queues and the kernel's static shared
+// memory (kVerifyWinSmemMax, gb_internal.h); a large halo shrinks the tile
 uint32_t verify_tile_words(uint32_t halo)
 {
-    if (kSlots * 2 * 4ull * (halo + kTileWords + kWinSlackWords) <= kVerifyDynSmemMax) return kTileWords;
-    const uint32_t tw = (kVerifyDynSmemMax / (8 * kSlots) - halo - kWinSlackWords) & ~127u;   // multiple of 128 words
+    if (2 * 4ull * (halo + kTileWords + kWinSlackWords) <= kVerifyWinSmemMax) return kTileWords;
+    const uint32_t tw = (kVerifyWinSmemMax / 8 - halo - kWinSlackWords) & ~127u;   // multiple of 128 words
     return tw;
 }
-constexpr size_t kQueueBytes = kMarkWarps * 128 * 6;   // per-warp survivor queues (u32 U + u16 index)
 size_t verify_smem(uint32_t halo)
 {
-    return kSlots * 2 * 4ull * (halo + verify_tile_words(halo) + kWinSlackWords) + kQueueBytes;
+    return 2 * 4ull * (halo + verify_tile_words(halo) + kWinSlackWords) + kQueueBytes;
 }
 
 SievePrimes sieve_primes(const gb_ctx *c, uint64_t sqrt_bound)
@@ -119,6 +117,19 @@ SievePrimes sieve_primes(const gb_ctx *c, uint64_t sqrt_bound)
     sp.i_big = count_le(c->h_primes, kWarpPrimeMax);
     sp.n_use = count_le(c->h_primes, sqrt_bound);
     return sp;
+}
+
+// the device that owns a device pointer (false for host / unregistered memory)
+bool pointer_device(const void *p, int &dev)
+{
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();                    // clear the sticky-free error state
+        return false;
+    }
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) return false;
+    dev = at.device;
+    return true;
 }
 
 struct DeviceGuard {
@@ -248,7 +259,7 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
         const uint32_t i_med = count_le(c->h_primes, 31), i_big = count_le(c->h_primes, kWarpPrimeMax);
         const uint32_t nmed = i_big > i_med ? i_big - i_med : 0;
         if (nmed > 1024) { delete c; return GB_EINTERNAL; }
-        const int nw = kSieveWarps;                    // warps that sieve (gb_verify.cu)
+        const int nw = kMarkWarps;                     // every warp of a verify CTA sieves
         const uint32_t h0 = verify_halo(c->h_primes[count_le(c->h_primes, p_max) - 1]);
         const double nbits = 32.0 * (h0 + verify_tile_words(h0));
         std::vector<std::vector<uint16_t>> lists(nw);
@@ -275,10 +286,8 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
             return GB_ECUDA;
         }
     }
-    // verify kernel smem limit for the largest p_max this ctx accepts
-    const uint32_t n_cand = count_le(c->h_primes, p_max);
-    const size_t smem_max = verify_smem(verify_halo(c->h_primes[n_cand - 1]));
-    if (configure_verify(smem_max) != cudaSuccess) { delete c; return GB_ECUDA; }
+    // verify kernel dynamic shared memory opt-in on this device
+    if (configure_verify() != cudaSuccess) { delete c; return GB_ECUDA; }
     *out = c;
     return GB_OK;
 }
@@ -335,9 +344,8 @@ gb_status gb_sieve_segment(gb_ctx *ctx, uint64_t word_lo, uint64_t n_words, uint
     a.lmask = nullptr;
     a.lmask_g0 = 0;
     a.lmask_stride = 0;
-    // two class windows + the TMA staging ring of base-prime tiles (2 x 1024 x 16 B;
-    // used by the GB_SIEVE_STAGED build)
-    const size_t smem = 4ull * ((2 * (a.tile_words + 1 + kWinSlackWords) + 3) & ~3ull) + 2 * 1024 * 16;
+    // the two class windows of a tile
+    const size_t smem = kSieveOutSmemMax;
     const int grid_max = (int)std::min<uint64_t>((uint64_t)ctx->num_sms, ctx->carry_ctas);
     const uint32_t i_large = count_le(ctx->h_primes, kCarryPrimeMax);
     const bool large = a.sp.n_use > i_large;
@@ -383,12 +391,18 @@ gb_status gb_sieve_segment(gb_ctx *ctx, uint64_t word_lo, uint64_t n_words, uint
 gb_status gb_result_init(int64_t *d_result, void *stream)
 {
     if (!d_result || ((uintptr_t)d_result & 7)) return GB_EINVAL;
+    int dev = -1;
+    if (!pointer_device(d_result, dev)) return GB_EINVAL;
+    DeviceGuard g(dev);
     return launch_result_init(d_result, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
 }
 
 gb_status gb_result_finalize(int64_t *d_result, void *stream)
 {
     if (!d_result || ((uintptr_t)d_result & 7)) return GB_EINVAL;
+    int dev = -1;
+    if (!pointer_device(d_result, dev)) return GB_EINVAL;
+    DeviceGuard g(dev);
     return launch_result_finalize(d_result, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
 }
 
@@ -624,6 +638,10 @@ gb_status gb_single_check(gb_ctx *ctx, uint64_t n, uint64_t p_limit, uint64_t *d
 gb_status gb_is_prime_u64(const uint64_t *d_x, uint8_t *d_out, uint64_t n, void *stream)
 {
     if (n && (!d_x || !d_out || ((uintptr_t)d_x & 7))) return GB_EINVAL;
+    if (n == 0) return GB_OK;
+    int dev = -1;
+    if (!pointer_device(d_x, dev)) return GB_EINVAL;
+    DeviceGuard g(dev);
     return launch_is_prime(d_x, d_out, n, nullptr, 0, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
 }
 

@@ -106,6 +106,7 @@ __device__ __forceinline__ uint32_t bin_of_prime(uint64_t p, const uint32_t *pri
 struct Acc {
     uint64_t evens = 0, verified = 0, fast_unres = 0, unres = 0, sum = 0, chk = 0;
     uint64_t key = 0, first_unres = UINT64_MAX;
+    uint64_t praw = 0;        // largest p_min above GB_KEY_PMAX (the key's p field saturates)
 };
 
 // End of a kernel: warp-reduce a thread's accumulators, then one atomic per warp per
@@ -126,7 +127,7 @@ __device__ __forceinline__ void flush_acc(const Acc &acc, int64_t *result, int l
     };
     const uint64_t ev = wsum(acc.evens), vf = wsum(acc.verified), fu = wsum(acc.fast_unres);
     const uint64_t un = wsum(acc.unres), sm = wsum(acc.sum), ck = wsum(acc.chk);
-    const uint64_t ky = wmax(acc.key), fr = wmin(acc.first_unres);
+    const uint64_t ky = wmax(acc.key), fr = wmin(acc.first_unres), pr = wmax(acc.praw);
     unsigned long long *R = (unsigned long long *)result;
     if (lane == 0) {
         if (ev) atomicAdd(R + GB_R_EVENS, ev);
@@ -136,6 +137,7 @@ __device__ __forceinline__ void flush_acc(const Acc &acc, int64_t *result, int l
         if (sm) atomicAdd(R + GB_R_SUM_PMIN, sm);
         if (ck) atomicAdd(R + GB_R_CHK_RAW, ck);
         if (ky) atomicMax(R + GB_R_MAX_KEY, ky);
+        if (pr) atomicMax(R + GB_R_MAX_PMIN_RAW, pr);
         if (fr != UINT64_MAX) atomicMin(R + GB_R_FIRST_UNRESOLVED_N, fr);
     }
 }
@@ -143,9 +145,18 @@ __device__ __forceinline__ void flush_acc(const Acc &acc, int64_t *result, int l
 // GB_R_MAX_KEY encoding: largest p first, then the smallest n
 __device__ __forceinline__ uint64_t make_key(uint64_t p, uint64_t n, uint64_t origin)
 {
-    const uint64_t pk = p < (1ull << 23) ? p : (1ull << 23) - 1;
+    const uint64_t pk = p < GB_KEY_PMAX ? p : GB_KEY_PMAX;
     const uint64_t idx = (n - origin) >> 1;
     return (pk << GB_KEY_SHIFT) | ((1ull << GB_KEY_SHIFT) - 1 - idx);
+}
+
+// fold (p_min, n) into a thread's running max key (and the raw max p_min when the
+// key's p field saturates)
+__device__ __forceinline__ void note_key(Acc &acc, uint64_t p, uint64_t n, uint64_t origin)
+{
+    const uint64_t key = make_key(p, n, origin);
+    if (key > acc.key) acc.key = key;
+    if (p >= GB_KEY_PMAX && p > acc.praw) acc.praw = p;
 }
 
 __device__ __forceinline__ void hist_add(uint32_t *sh_hist, int64_t *res, uint32_t bin, uint32_t c)

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <vector>
 
 #include "gb.h"
@@ -11,52 +12,31 @@
 namespace gb {
 
 // ---- tiling constants (tuned for sm_100a: 148 SMs, 228 KB smem / SM) ----
-#ifndef GB_THREADS
-#define GB_THREADS 1024
-#endif
-constexpr int kThreads = GB_THREADS;       // threads per CTA, every kernel
-// Warp specialization of the verify kernel (GB_WS=1, an A/B option): kSieveWarps
-// warps sieve tile t+1 into one window slot while the other warps mark tile t from
-// the other slot (two half-size slots).  Measured slower than the default: at best
-// 42.8 ms (16 sieving warps) vs 38.3 ms on the 2^36 profile span -- the sieve is
-// latency bound and scales with its warp count, and half tiles double the
-// per-prime work per even.
-#ifndef GB_WS
-#define GB_WS 0
-#endif
-#ifndef GB_SIEVE_WARPS
-#define GB_SIEVE_WARPS 12
-#endif
-#ifndef GB_TILE_WORDS
-#if GB_WS
-#define GB_TILE_WORDS 10240
-#else
-#define GB_TILE_WORDS 20480
-#endif
-#endif
-constexpr int kTileWords = GB_TILE_WORDS;  // verify tile: 32-bit words per mod-6 class
-constexpr int kSlots = GB_WS ? 2 : 1;      // window slots of the verify kernel
-constexpr int kSieveWarps = GB_WS ? GB_SIEVE_WARPS : GB_THREADS / 32;   // warps that sieve (medium LPT schedule)
-constexpr int kMarkWarps = GB_WS ? GB_THREADS / 32 - GB_SIEVE_WARPS : GB_THREADS / 32;   // warps that mark
-constexpr uint32_t kTileM = 32u * kTileWords;  // m-span of a tile (n = 6m + a): 786432 evens
+constexpr int kThreads = 1024;             // threads per CTA, every kernel (768 / 896: slower)
+constexpr int kTileWords = 20480;          // verify tile: 32-bit words per mod-6 class
+constexpr int kMarkWarps = kThreads / 32;  // warps of a verify CTA (each sieves, then marks)
+constexpr uint32_t kTileM = 32u * kTileWords;  // m-span of a tile (n = 6m + a): 655360 m per class
+// verify kernel dynamic shared memory: the two class windows (halo + tile + slack
+// words each, <= kVerifyWinSmemMax) + per-warp survivor queues (u32 U + u16 index)
+constexpr uint32_t kVerifyWinSmemMax = 168 * 1024;
+constexpr uint32_t kWinSlackWords = 128;      // words past a window phase-1 lanes may read (U = 0)
+constexpr uint32_t kQueueEntries = 128;       // per-warp survivor queue
+constexpr size_t kQueueBytes = (size_t)kMarkWarps * kQueueEntries * 6;
+constexpr size_t kVerifySmemMax = kVerifyWinSmemMax + kQueueBytes;
+// sieve_out_kernel: the two class windows of one tile (+ one word) + slack
+constexpr size_t kSieveOutSmemMax = 4ull * ((2 * (kTileWords + 1 + kWinSlackWords) + 3) & ~3ull);
 constexpr int kSieveTileWords = 16384;     // 32-bit words per gb_sieve_segment CTA
 constexpr int kHistSmem = 1024;            // histogram bins kept in shared memory
-#ifndef GB_WARP_PMAX
-#define GB_WARP_PMAX 8192
-#endif
-constexpr uint32_t kWarpPrimeMax = GB_WARP_PMAX;   // primes <= this: one warp per prime
+constexpr uint32_t kWarpPrimeMax = 8192;   // primes <= this: one warp per prime (4096: slower)
 constexpr int kTinyPrimes = 10;            // 3..31 sieved by word patterns
 constexpr uint64_t kDumpScratch = 1ull << 24;  // u32 entries of host-API dump scratch
 constexpr int kScanBlockWords = 2048;      // u64 words per K-BASE compaction block
 constexpr uint32_t kCarryPrimeMax = 1u << 21;  // verify CTAs carry sieve offsets of primes below
 constexpr int kMaxBlocksPerSm = 4;         // sizing bound for per-CTA carry storage
-#ifndef GB_LARGE_TILES_PER_SM
-#define GB_LARGE_TILES_PER_SM (GB_WS ? 6 : 3)
-#endif
 // Ranges that need sieving primes above kCarryPrimeMax (hi > 2^42, e.g. the 4e18
-// window) run in chunks of GB_LARGE_TILES_PER_SM verify tiles per SM; before each
+// window) run in chunks of kLargeTilesPerSm verify tiles per SM; before each
 // chunk K-LARGE marks the multiples of those primes into an L2-resident wheel mask.
-constexpr int kLargeTilesPerSm = GB_LARGE_TILES_PER_SM;
+constexpr int kLargeTilesPerSm = 3;
 
 // Arguments of the window sieve (K-SIEVE) shared by every caller.
 struct SievePrimes {
@@ -179,7 +159,8 @@ cudaError_t launch_verify(const VerifyArgs &a, int grid, size_t smem, cudaStream
 cudaError_t launch_large(const LargeArgs &a, int num_sms, cudaStream_t st);   // mask fill + marking
 cudaError_t launch_is_prime(const uint64_t *x, uint8_t *out, uint64_t n, const uint64_t *bits,
                             uint64_t R, cudaStream_t st);
-cudaError_t configure_verify(size_t smem_max);
+cudaError_t configure_verify();
+cudaError_t ensure_dyn_smem(const void *kernel, int bytes, std::atomic<uint64_t> &done);
 cudaError_t launch_sieve_out(const SieveOutArgs &a, int grid, size_t smem, cudaStream_t st);
 int verify_blocks_per_sm(size_t smem);
 uint32_t unroll_p_max();       // largest prime of the unrolled class tables

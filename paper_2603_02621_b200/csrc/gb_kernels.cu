@@ -22,6 +22,21 @@ namespace gb {
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// cudaFuncSetAttribute applies to the current device's context only: opt each
+// kernel in once per device (bit d of `done`), always to the largest size it is
+// ever launched with, so no later call can lower it under another context's feet.
+cudaError_t ensure_dyn_smem(const void *kernel, int bytes, std::atomic<uint64_t> &done)
+{
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+    return e;
+}
 }  // namespace gb
 
 extern "C" uint64_t gb_launch_count(void) { return gb::g_launches.load(); }
@@ -267,11 +282,6 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint64_t *bits, uint
 // kernel ANDs the mask into its windows.  The prime table is streamed with
 // evict-first loads so it does not push the mask out of L2.
 // ---------------------------------------------------------------------------
-#ifndef GB_LARGE_NOHINT
-#define GB_LARGE_HINT 1
-#else
-#define GB_LARGE_HINT 0
-#endif
 // L2 policy for the chunk mask: keep it resident (evict_last) while the prime table
 // streams through with evict-first loads
 __device__ __forceinline__ uint64_t l2_keep_policy()
@@ -284,132 +294,21 @@ __device__ __forceinline__ uint64_t l2_keep_policy()
 __global__ void __launch_bounds__(256) large_fill_kernel(uint32_t *mask, uint64_t stride, uint32_t nw)
 {
     const uint64_t n = stride + nw;             // class A [0, nw) .. class B [stride, stride + nw)
-#if GB_LARGE_HINT
     const uint64_t pol = l2_keep_policy();
-#endif
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-#if GB_LARGE_HINT
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(mask + i), "r"(0xFFFFFFFFu), "l"(pol)
                      : "memory");
-#else
-        mask[i] = 0xFFFFFFFFu;
-#endif
-    }
 }
 
 __device__ __forceinline__ void gmem_and(uint32_t *p, uint32_t v, uint64_t pol)
 {
-#if GB_LARGE_HINT
     asm volatile("red.global.and.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
-#else
-    asm volatile("red.global.and.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-#endif
 }
 
-#ifndef GB_LARGE_ILP
-#define GB_LARGE_ILP 2
-#endif
-#ifndef GB_LARGE_BLOCK
-#define GB_LARGE_BLOCK 256
-#endif
-#ifndef GB_LARGE_GRID_PER_SM
-#define GB_LARGE_GRID_PER_SM 64
-#endif
-constexpr int kLargeIlp = GB_LARGE_ILP;        // primes in flight per thread
-constexpr int kLargeBlock = GB_LARGE_BLOCK;
+constexpr int kLargeBlock = 256;
+constexpr int kLargeGridPerSm = 64;
 
-// first hits (bits relative to the mask start) of prime p in class A and class B,
-// or >= nbits; the masks are < 2^30 bits, so offsets are 32-bit
-// x mod p through a double-precision quotient estimate, within a few units of the
-// true quotient while x / p < 2^45 (K-LARGE: x < 2^60, p > 2^21); an A/B option
-// (GB_LARGE_FP64MOD) that drops the reciprocal-table reads -- measured no faster
-__device__ __forceinline__ uint32_t mod_fp64(uint64_t x, uint32_t p)
-{
-    const int64_t q = (int64_t)__dmul_rn((double)x, __drcp_rn((double)p));
-    int64_t r = (int64_t)(x - (uint64_t)q * p);
-    while (r < 0) r += p;
-    while (r >= (int64_t)p) r -= p;
-    return (uint32_t)r;
-}
-
-__device__ __forceinline__ void large_first_hits(uint32_t p, const uint64_t *magic_ptr, int64_t m_lo, int64_t m_hi,
-                                                 uint32_t nbits, uint32_t &bA, uint32_t &bB)
-{
-    bA = bB = nbits;
-    // the first multiple cleared is p^2 (= 6m + 1, class A): p itself stays set
-    const int64_t mmin = (int64_t)(((uint64_t)p * p - 1) / 6);
-    if (mmin >= m_hi) return;
-    const uint64_t ms = (uint64_t)(mmin > m_lo ? mmin : m_lo);
-#ifdef GB_LARGE_FP64MOD
-    (void)magic_ptr;
-    const uint32_t rem = mod_fp64(ms, p);
-#else
-    const uint32_t rem = mod_magic(ms, p, __ldcs(magic_ptr));
-#endif
-    // m with p | 6m+1: m == -1/6 (mod p); p | 6m+5: m == -5/6 (mod p)
-    const uint64_t inv6 = (p % 6 == 1) ? (5ull * p + 1) / 6 : ((uint64_t)p + 1) / 6;
-    const uint32_t rA = p - (uint32_t)inv6;
-    uint64_t t = 5ull * rA;
-    while (t >= p) t -= p;
-    const uint32_t rB = (uint32_t)t;
-    const uint64_t base = ms - (uint64_t)m_lo;
-    const uint64_t xA = base + (rA >= rem ? rA - rem : rA + p - rem);
-    const uint64_t xB = base + (rB >= rem ? rB - rem : rB + p - rem);
-    if (xA < nbits) bA = (uint32_t)xA;
-    if (xB < nbits) bB = (uint32_t)xB;
-}
-
-// next hit of a progression: b + p (no 32-bit overflow: b < 2^30, and p >= 2^31
-// has a single hit in any mask)
-__device__ __forceinline__ uint32_t large_next(uint32_t b, uint32_t p, uint32_t nbits)
-{
-    return p >= 0x80000000u ? nbits : b + p;
-}
-
-__global__ void __launch_bounds__(kLargeBlock) large_mark_kernel(LargeArgs a)
-{
-    const int64_t m_lo = a.g0 * 32;
-    const int64_t m_hi = m_lo + 32 * (int64_t)a.nw;
-    const uint32_t nbits = 32 * a.nw;
-    const uint64_t n = a.i_end - a.i_begin;
-    const uint64_t total = (uint64_t)gridDim.x * blockDim.x;
-    uint32_t *__restrict__ mA = a.mask;
-    uint32_t *__restrict__ mB = a.mask + a.stride;
-    const uint64_t pol = GB_LARGE_HINT ? l2_keep_policy() : 0;
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += kLargeIlp * total) {
-        uint32_t bA[kLargeIlp], bB[kLargeIlp], pp[kLargeIlp];
-#pragma unroll
-        for (int j = 0; j < kLargeIlp; ++j) {
-            const uint64_t kk = k + j * total;
-            pp[j] = 1;
-            bA[j] = bB[j] = nbits;
-            if (kk < n) {
-                const uint32_t pi = a.i_begin + (uint32_t)kk;
-                pp[j] = __ldcs(a.primes + pi);
-                large_first_hits(pp[j], a.magic + pi, m_lo, m_hi, nbits, bA[j], bB[j]);
-            }
-        }
-        // all progressions of this thread advance together (one loop, predicated REDs)
-        bool more = true;
-        while (more) {
-            more = false;
-#pragma unroll
-            for (int j = 0; j < kLargeIlp; ++j) {
-                if (bA[j] < nbits) {
-                    gmem_and(mA + (bA[j] >> 5), clear_mask(bA[j]), pol);
-                    bA[j] = large_next(bA[j], pp[j], nbits);
-                }
-                if (bB[j] < nbits) {
-                    gmem_and(mB + (bB[j] >> 5), clear_mask(bB[j]), pol);
-                    bB[j] = large_next(bB[j], pp[j], nbits);
-                }
-                more |= (bA[j] < nbits) | (bB[j] < nbits);
-            }
-        }
-    }
-}
-
-// K-LARGE with a cofactor wheel (default).  A bit q = p k of the mask needs
+// K-LARGE with a cofactor wheel.  A bit q = p k of the mask needs
 // clearing only if no other sieve clears it: the window's shared-memory sieve
 // clears every q with a prime factor <= 2^21 (q >= f^2 always holds here), so a
 // multiple whose cofactor k has a factor 5, 7, 11, 13, 17 or 19 is cleared anyway
@@ -453,13 +352,13 @@ __global__ void __launch_bounds__(kLargeBlock) large_mark_wheel_kernel(LargeArgs
     // offsets off = q - q_base, m = off / 6; q_base = 6 m_lo wraps mod 2^64 when
     // m_lo < 0 (ranges starting below the halo), and exceeds INT64_MAX near 2^64
     const uint64_t q_base = 6 * (uint64_t)m_lo;
-    const uint64_t lim_off = 6ull * nbits;                 // < 2^32 (nbits < 2^30 / 3)
+    const uint64_t lim_off = 6ull * nbits;                 // < 2^32 (launch_large checks 192 nw < 2^32)
     const uint64_t q_first = m_lo > 0 ? q_base : 0;
     const uint64_t n = a.i_end - a.i_begin;
     const uint64_t total = (uint64_t)gridDim.x * blockDim.x;
     uint32_t *__restrict__ mA = a.mask;
     uint32_t *__restrict__ mB = a.mask + a.stride;
-    const uint64_t pol = GB_LARGE_HINT ? l2_keep_policy() : 0;
+    const uint64_t pol = l2_keep_policy();
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += total) {
         const uint32_t pi = a.i_begin + (uint32_t)t;
         const uint64_t p = __ldcs(a.primes + pi);
@@ -534,8 +433,8 @@ __global__ void is_prime_kernel(const uint64_t *x, uint8_t *out, uint64_t n)
 cudaError_t launch_seed(uint64_t s, uint32_t *primes, uint64_t *magic, uint4 *pk,
                         uint32_t *d_count, cudaStream_t st)
 {
-    static const cudaError_t attr = cudaFuncSetAttribute(
-        seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 16);
+    static std::atomic<uint64_t> done{0};
+    const cudaError_t attr = ensure_dyn_smem((const void *)seed_kernel, 65536 + 16, done);
     if (attr != cudaSuccess) return attr;
     seed_kernel<<<1, 1024, (size_t)s + 1, st>>>((uint32_t)s, primes, magic, pk, d_count);
     count_launch();
@@ -546,8 +445,8 @@ cudaError_t launch_segment(const SegmentArgs &a, cudaStream_t st)
 {
     const uint64_t nb = (a.n_words32 + kSieveTileWords - 1) / kSieveTileWords;
     if (nb == 0) return cudaSuccess;
-    static const cudaError_t attr = cudaFuncSetAttribute(
-        segment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSieveTileWords * 4);
+    static std::atomic<uint64_t> done{0};
+    const cudaError_t attr = ensure_dyn_smem((const void *)segment_kernel, kSieveTileWords * 4, done);
     if (attr != cudaSuccess) return attr;
     segment_kernel<<<(unsigned)nb, kThreads, kSieveTileWords * 4, st>>>(a);
     count_launch();
@@ -585,13 +484,10 @@ cudaError_t launch_large(const LargeArgs &a, int num_sms, cudaStream_t st)
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || a.i_end <= a.i_begin) return e;
     const uint64_t n = a.i_end - a.i_begin;
-    if (a.nw >= (1u << 25)) return cudaErrorInvalidValue;      // 32-bit bit offsets (< 2^30)
-    const uint64_t nb = std::min<uint64_t>((n + kLargeBlock - 1) / kLargeBlock, (uint64_t)GB_LARGE_GRID_PER_SM * num_sms);
-#ifdef GB_LARGE_NOWHEEL
-    large_mark_kernel<<<(unsigned)nb, kLargeBlock, 0, st>>>(a);
-#else
+    // large_mark_wheel_kernel keeps integer offsets 6 * 32 * nw in 32 bits
+    if ((uint64_t)a.nw * 192 >= (1ull << 32)) return cudaErrorInvalidValue;
+    const uint64_t nb = std::min<uint64_t>((n + kLargeBlock - 1) / kLargeBlock, (uint64_t)kLargeGridPerSm * num_sms);
     large_mark_wheel_kernel<<<(unsigned)nb, kLargeBlock, 0, st>>>(a);
-#endif
     count_launch();
     return cudaGetLastError();
 }

@@ -97,8 +97,7 @@ __global__ void __launch_bounds__(256) pern_kernel(const __grid_constant__ PerNA
                 acc.verified += 1;
                 acc.sum += pmin;
                 acc.chk += pmin * (n / 192);                      // DESIGN.md R6 weight
-                const uint64_t key = make_key(pmin, n, a.origin);
-                if (key > acc.key) acc.key = key;
+                note_key(acc, pmin, n, a.origin);
                 hist_add(sh_hist, a.result, bin, 1);
             } else {
                 acc.unres += 1;

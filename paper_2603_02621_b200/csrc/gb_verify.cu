@@ -21,6 +21,7 @@
 // with s = 32a + b.
 #include <stdint.h>
 
+#include <atomic>
 #include <cstdio>
 
 #include "gb_device.cuh"
@@ -46,16 +47,10 @@ __host__ __device__ constexpr Trans trans(int a, uint32_t p)
     return b == 5 ? Trans{1, 1, j + 1} : Trans{0, 0, 0};
 }
 
-#ifndef GB_K6
-#define GB_K6 192
-#endif
-#ifndef GB_P1
-#define GB_P1 56
-#endif
-constexpr int kK = GB_K6;        // unrolled candidates per class
-constexpr int kP1 = GB_P1;       // phase 1: candidates every word goes through
-constexpr uint32_t kWinSlack = 128;   // words past a window that phase-1 lanes may read (U = 0)
-constexpr int kQueue = 128;      // per-warp survivor queue (<= 31 carried + 32 kW per round)
+constexpr int kK = 192;          // unrolled candidates per class
+constexpr int kP1 = 56;          // phase 1: candidates every word goes through
+constexpr uint32_t kWinSlack = kWinSlackWords;   // words past a window phase-1 lanes may read (U = 0)
+constexpr int kQueue = kQueueEntries;   // per-warp survivor queue (<= 31 carried + 32 kW per round)
 static_assert(kK % 8 == 0 && kP1 % 8 == 0 && kP1 <= kK, "blocks of 8 candidates");
 
 
@@ -163,9 +158,6 @@ __device__ __forceinline__ void clear_bit(uint32_t w, uint32_t b)
     smem_and(w + ((b >> 5) << 2), clear_mask(b));
 }
 
-#ifndef GB_MP2_UNROLL
-#define GB_MP2_UNROLL 2
-#endif
 // One warp, one medium prime, both classes: lane l marks hits l, l + 32, ... of each
 // class (bits off + (l + 32i) p).  The stride is p whole words, so a lane's bit-in-
 // word (hence its mask) never changes: only the word address moves, by 4p bytes per
@@ -181,26 +173,12 @@ __device__ __forceinline__ void mark_progression2(uint32_t wA, uint32_t offA, ui
     uint32_t adA = wA + ((bA >> 5) << 2), adB = wB + ((bB >> 5) << 2);
     const uint32_t n = min(nA, nB);
     uint32_t i = 0;
-#if GB_MP2_UNROLL >= 4
-    for (; i + 4 <= n; i += 4, adA += 4 * step, adB += 4 * step) {
-        smem_and(adA, mA);
-        smem_and(adB, mB);
-        smem_and(adA + step, mA);
-        smem_and(adB + step, mB);
-        smem_and(adA + 2 * step, mA);
-        smem_and(adB + 2 * step, mB);
-        smem_and(adA + 3 * step, mA);
-        smem_and(adB + 3 * step, mB);
-    }
-#endif
-#if GB_MP2_UNROLL >= 2
     for (; i + 2 <= n; i += 2, adA += 2 * step, adB += 2 * step) {
         smem_and(adA, mA);
         smem_and(adB, mB);
         smem_and(adA + step, mA);
         smem_and(adB + step, mB);
     }
-#endif
     for (; i < n; ++i, adA += step, adB += step) {
         smem_and(adA, mA);
         smem_and(adB, mB);
@@ -211,105 +189,34 @@ __device__ __forceinline__ void mark_progression2(uint32_t wA, uint32_t offA, ui
 
 // Carried sieve offsets (per-CTA rows, ~92 MB at N = 1e12): L2 accesses with an
 // evict_last policy so the rows stay resident in L2 across tiles instead of making
-// a DRAM round trip per tile (GB_CARRY_NOHINT: plain .cg accesses, for A/B).
+// a DRAM round trip per tile (plain .cg accesses: DRAM reads 9.7 vs 2.0 GB per
+// 2^36-integer launch).
 __device__ __forceinline__ uint64_t carry_policy()
 {
-#ifdef GB_CARRY_NOHINT
-    return 0;
-#else
     uint64_t pol;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
-#endif
 }
 __device__ __forceinline__ uint32_t carry_ld(const uint32_t *p, uint64_t pol)
 {
-#ifdef GB_CARRY_NOHINT
-    (void)pol;
-    return __ldcg(p);
-#else
     uint32_t v;
     asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
     return v;
-#endif
 }
 __device__ __forceinline__ void carry_st(uint32_t *p, uint32_t v, uint64_t pol)
 {
-#ifdef GB_CARRY_NOHINT
-    (void)pol;
-    __stcg(p, v);
-#else
     asm volatile("st.global.cg.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
-#endif
 }
 
-// ---- TMA (cp.async.bulk) staging of base-prime tiles for the standalone sieve ----
-constexpr uint32_t kStagePrimes = 1024;         // primes per staged tile (16 B each): 16 KB
-constexpr uint32_t kStageBufs = 2;              // ring depth (32 KB)
-// gb_sieve_segment with TMA-staged base-prime tiles (GB_SIEVE_STAGED=1) is an A/B
-// option: parity-green (the sieve tests pass on that build) but measured slower than
-// the __ldg path with 2 primes in flight per thread -- 5.82 vs 5.31 ms per 2^34
-// integers at 1e12, 19.2 vs 18.8 ms at 4e18.
-#ifdef GB_SIEVE_STAGED
-constexpr bool kSieveStaged = true;
-#else
-constexpr bool kSieveStaged = false;
-#endif
-struct TmaStage {
-    uint4 *buf;                                 // kStageBufs x kStagePrimes (p, tile_m mod p, rA, rB)
-    uint64_t *bar;                              // kStageBufs "full" mbarriers (TMA transaction count)
-    uint32_t *done;                             // kStageBufs counters of warps done with the buffer
-    uint32_t uses[kStageBufs];                  // completed phases per buffer (parity)
-};
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init()
-{
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-// one thread: arm the barrier with the byte count and start the bulk copy global -> shared
-__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
-{
-    uint32_t done;
-    do {
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-                     " selp.u32 %0, 1, 0, p;\n}\n"
-                     : "=r"(done)
-                     : "r"(smem_addr(bar)), "r"(parity)
-                     : "memory");
-    } while (!done);
-}
 
-// barrier of the NT threads that run sieve6_window: the whole CTA, or (warp-
-// specialized verify kernel) the sieving warps 0 .. NT/32-1 on named barrier 1
-template <int NT>
-__device__ __forceinline__ void group_sync()
-{
-    if constexpr (NT == kThreads) __syncthreads();
-    else asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
-}
-
-// K-SIEVE of one tile's two class windows by NT threads (gtid = 0 .. NT-1, whole
-// warps); ends WITHOUT a barrier
-template <bool DEF_TILE, int NT, bool STAGED = false>
+// K-SIEVE of one tile's two class windows by the whole CTA; ends WITHOUT a barrier
+template <bool DEF_TILE>
 __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
                               Carry6 *cy, const MedSched &ms, uint32_t i_b2, uint32_t i_b1,
-                              const uint32_t *__restrict__ lm, int64_t lg0, uint64_t lstride, int gtid,
-                              TmaStage *stg = nullptr)
+                              const uint32_t *__restrict__ lm, int64_t lg0, uint64_t lstride, int tid)
 {
-    const int tid = gtid;
     const uint32_t lane = (uint32_t)tid & 31;
-    constexpr int nt = NT;
+    constexpr int nt = kThreads;
     const uint32_t sA = smem_addr(wA), sB = smem_addr(wB);
     if (cy->init) {
         // first tile of this CTA's run: carried offsets of the steady primes by modulo
@@ -322,7 +229,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             carry_st(cy->off + pi, oa, ipol);
             carry_st(cy->off + cy->stride + pi, ob, ipol);
         }
-        group_sync<NT>();
+        __syncthreads();
     }
     // Phase T: primes 5..31 by shifted word patterns, per-thread incremental phases
     {
@@ -418,10 +325,10 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
         sh_hA[pi - sp.i_med] = (uint16_t)(oa < nbits ? (nbits - oa + k.x - 1) / k.x : 0);
         sh_hB[pi - sp.i_med] = (uint16_t)(ob < nbits ? (nbits - ob + k.x - 1) / k.x : 0);
     }
-    group_sync<NT>();
+    __syncthreads();
     // one warp per medium prime: the host's LPT schedule (longest work first onto
     // the least-loaded warp) gives every sieving warp the same share, no atomics
-    if ((uint32_t)tid < 32u * kSieveWarps) {
+    {
         const uint32_t warp = (uint32_t)tid >> 5;
         const uint32_t k0 = __ldg(ms.off + warp), k1 = __ldg(ms.off + warp + 1);
         for (uint32_t k = k0; k < k1; ++k) {
@@ -441,56 +348,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
     uint32_t *__restrict__ cA = cy->off;                 // this CTA's carry row, class A
     uint32_t *__restrict__ cB = cy->off + cy->stride;    // class B
     const uint4 *__restrict__ pkp = sp.pk;
-#ifndef GB_KB
-#define GB_KB 2
-#endif
-    constexpr int kB = GB_KB;
-    if constexpr (STAGED) {
-        // steady primes from TMA-staged tiles of their constants (cp.async.bulk into a
-        // ring of kStageBufs shared buffers, completion on an mbarrier): thread t takes
-        // prime t of the tile, both classes, by the same three regimes as below.  The
-        // last warp done with a buffer refills it, so no CTA-wide barrier is needed.
-        static_assert(NT == kStagePrimes, "one prime per thread");
-        const uint32_t n_st = s_end - b_begin;
-        const uint32_t nch = (n_st + kStagePrimes - 1) / kStagePrimes;
-        auto issue = [&](uint32_t c) {
-            const uint32_t cnt = min(kStagePrimes, n_st - c * kStagePrimes);
-            tma_load_1d(stg->buf + (c % kStageBufs) * kStagePrimes, sp.pk + b_begin + c * kStagePrimes, 16 * cnt,
-                        stg->bar + (c % kStageBufs));
-        };
-        if (tid == 0)
-            for (uint32_t c = 0; c < kStageBufs && c < nch; ++c) issue(c);
-        for (uint32_t c = 0; c < nch; ++c) {
-            const uint32_t b = c % kStageBufs;
-            mbar_wait(stg->bar + b, stg->uses[b] & 1);
-            ++stg->uses[b];
-            const uint32_t pi = b_begin + c * kStagePrimes + (uint32_t)tid;
-            uint4 q = make_uint4(1, 0, 0, 0);
-            if (pi < s_end) q = stg->buf[b * kStagePrimes + tid];
-            __syncwarp();
-            if (lane == 0 && atomicAdd(stg->done + b, 1u) == NT / 32 - 1) {   // last warp out
-                stg->done[b] = 0;
-                if (c + kStageBufs < nch) issue(c + kStageBufs);
-            }
-            if (pi < s_end) {
-                const uint32_t p = q.x, tm = tile_mod<DEF_TILE>(cy, q);
-                const uint32_t oa = carry_ld(cA + pi, cpol), ob = carry_ld(cB + pi, cpol);
-                if (pi < b2) {                                   // >= 2 hits per class
-                    for (uint32_t bb = oa; bb < nbits; bb += p) clear_bit(sA, bb);
-                    for (uint32_t bb = ob; bb < nbits; bb += p) clear_bit(sB, bb);
-                } else {                                         // <= 2 (or <= 1) hits per class
-                    if (oa < nbits) clear_bit(sA, oa);
-                    if (ob < nbits) clear_bit(sB, ob);
-                    if (pi < b1) {
-                        if (oa + p < nbits) clear_bit(sA, oa + p);
-                        if (ob + p < nbits) clear_bit(sB, ob + p);
-                    }
-                }
-                carry_st(cA + pi, oa >= tm ? oa - tm : oa + p - tm, cpol);
-                carry_st(cB + pi, ob >= tm ? ob - tm : ob + p - tm, cpol);
-            }
-        }
-    } else {
+    constexpr int kB = 2;             // steady primes in flight per thread (1 or 4: slower)
     // steady primes with p <= full window / 2: hit loops (>= 2 hits per class)
     for (uint32_t w0 = b_begin + (tid & ~31u); w0 < b2; w0 += kB * nt) {   // warp-uniform trips
         const uint32_t p0 = w0 + lane;
@@ -512,20 +370,14 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
 #pragma unroll
         for (int k = 0; k < kB; ++k) {
             const uint32_t p = pt[k].x, tm = pt[k].y;
-#ifdef GB_MULTI_SPLIT
-            for (uint32_t b = oa[k]; b < nbits; b += p) clear_bit(sA, b);
-            for (uint32_t b = ob[k]; b < nbits; b += p) clear_bit(sB, b);
-#else
             {   // both classes in one loop (hit counts differ by at most one)
                 uint32_t ba = oa[k], bb = ob[k];
-#ifndef GB_MH_NOUNROLL
                 for (; ba + p < nbits && bb + p < nbits; ba += 2 * p, bb += 2 * p) {   // 2 hits per class
                     clear_bit(sA, ba);
                     clear_bit(sB, bb);
                     clear_bit(sA, ba + p);
                     clear_bit(sB, bb + p);
                 }
-#endif
                 for (; ba < nbits && bb < nbits; ba += p, bb += p) {
                     clear_bit(sA, ba);
                     clear_bit(sB, bb);
@@ -533,7 +385,6 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
                 for (; ba < nbits; ba += p) clear_bit(sA, ba);
                 for (; bb < nbits; bb += p) clear_bit(sB, bb);
             }
-#endif
             const uint32_t pi = p0 + k * nt;
             if (pi < b2) {
                 carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
@@ -543,10 +394,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
         __syncwarp();   // reconverge: the per-lane hit loops diverge
     }
     // steady primes with window/2 < p <= window: at most 2 hits per class, predicated
-#ifndef GB_KB2
-#define GB_KB2 2
-#endif
-    constexpr int kB2 = GB_KB2;
+    constexpr int kB2 = 2;
     for (uint32_t w0 = b2 + (tid & ~31u); w0 < b1; w0 += kB2 * nt) {
         const uint32_t p0 = w0 + lane;
         uint32_t pp[kB2], tt[kB2], oa[kB2], ob[kB2];
@@ -607,7 +455,6 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
                 carry_st(cB + pi, ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm, cpol);
             }
         }
-    }
     }
     for (uint32_t pi = s_end + tid; pi < sp.n_use; pi += nt) {
         const uint4 k = __ldg(sp.pk + pi);
@@ -727,10 +574,7 @@ __device__ __forceinline__ void phase1(Lane6 &m0, Lane6 &m1, uint32_t *h, int la
 }
 
 // ---- phase 1 with kW words per lane (words li, li + 32, ..., li + 32(kW-1)) ----
-#ifndef GB_W1
-#define GB_W1 3
-#endif
-constexpr int kW = GB_W1;
+constexpr int kW = 3;            // phase-1 words per lane (2: slower)
 static_assert(kW * 32 * 32 < 65536, "16-bit packed per-warp counts");
 static_assert(31 + 32 * kW <= kQueue, "survivor queue capacity");
 
@@ -812,10 +656,7 @@ __device__ __forceinline__ void phase1q(LaneQ &m, uint32_t *h, int lane)
 // words per lane (a round's survivors gathered through the warp's queue area), so
 // candidates kC1 .. kP1-1 run only on live words.  Word k of a lane has its own
 // window position li[k].
-#ifndef GB_C1
-#define GB_C1 40
-#endif
-constexpr int kC1 = GB_C1;
+constexpr int kC1 = 40;          // compaction point (24/32/48: slower)
 static_assert(kC1 % 8 == 0 && kC1 <= kP1, "compaction point on a block boundary");
 
 template <int S>
@@ -931,8 +772,7 @@ __device__ __forceinline__ void replay_key(const Lane6 &m, uint64_t u, const Ver
         if (nw) { lp = p; lbits = nw; }
     }
     const uint64_t n = 6 * (u * 32 + (uint64_t)(__ffs(lbits) - 1)) + A;
-    const uint64_t key = make_key(lp, n, a.origin);
-    if (key > acc.key) acc.key = key;
+    note_key(acc, lp, n, a.origin);
 }
 
 template <int A>
@@ -963,8 +803,7 @@ __device__ __forceinline__ void replay_key_q(const LaneQ &m, uint64_t u0w, const
             if (nw) { lp = p; lbits = nw; }
         }
         const uint64_t n = 6 * ((u0w + 32 * k) * 32 + (uint64_t)(__ffs(lbits) - 1)) + A;
-        const uint64_t key = make_key(lp, n, a.origin);
-        if (key > acc.key) acc.key = key;
+        note_key(acc, lp, n, a.origin);
     }
 }
 
@@ -996,8 +835,7 @@ __device__ __forceinline__ void replay_key_r(const LaneR<S> &m, uint64_t u0, con
             if (nw) { lp = p; lbits = nw; }
         }
         const uint64_t n = 6 * ((u0 + m.li[k]) * 32 + (uint64_t)(__ffs(lbits) - 1)) + A;
-        const uint64_t key = make_key(lp, n, a.origin);
-        if (key > acc.key) acc.key = key;
+        note_key(acc, lp, n, a.origin);
     }
 }
 
@@ -1037,8 +875,7 @@ __device__ __forceinline__ void finish_word(uint32_t U, uint64_t word_sum, uint3
     }
     if (lastp) {
         const uint64_t n = 6 * (u * 32 + (uint64_t)(__ffs(lastb) - 1)) + A;
-        const uint64_t key = make_key(lastp, n, a.origin);
-        if (key > acc.key) acc.key = key;
+        note_key(acc, lastp, n, a.origin);
     }
     acc.fast_unres += __popc(U);
     while (true) {
@@ -1055,8 +892,7 @@ __device__ __forceinline__ void finish_word(uint32_t U, uint64_t word_sum, uint3
             if (p) {
                 word_sum += p;
                 hist_add(sh_hist, a.result, bin_of_prime(p, a.sp.primes, a.n_base), 1);
-                const uint64_t key = make_key(p, n, a.origin);
-                if (key > acc.key) acc.key = key;
+                note_key(acc, p, n, a.origin);
             } else {
                 acc.unres += 1;
                 hist_add(sh_hist, a.result, 0, 1);
@@ -1090,16 +926,14 @@ __device__ __forceinline__ uint32_t take_special(uint32_t U, uint64_t u, uint32_
         U &= ~1u;
         acc.sum += 2;
         atomicAdd(sh_hist + 1, 1u);
-        const uint64_t key = make_key(2, 4, a.origin);
-        if (key > acc.key) acc.key = key;
+        note_key(acc, 2, 4, a.origin);
         if (DUMP) a.dump[(4 - a.lo_e) / 2] = 2;
     }
     if (A == 0 && (U & 2u)) {
         U &= ~2u;
         acc.sum += 3;
         atomicAdd(sh_hist + 2, 1u);
-        const uint64_t key = make_key(3, 6, a.origin);
-        if (key > acc.key) acc.key = key;
+        note_key(acc, 3, 6, a.origin);
         if (DUMP) a.dump[(6 - a.lo_e) / 2] = 3;
     }
     return U;
@@ -1206,11 +1040,7 @@ struct ClassWork {
         const uint64_t ub = u0 + pair * 32 * kW;
         const bool interior = pair * 32 * kW + 32 * kW <= tw && ub != 0 && ub * 32 >= a.m_lo[A / 2] &&
                               (ub + 32 * kW) * 32 <= a.m_hi[A / 2];
-#ifdef GB_NO_INTERIOR
-        if (false) {
-#else
         if (interior) {
-#endif
 #pragma unroll
             for (int k = 0; k < kW; ++k) {
                 m.U[k] = FULL;
@@ -1391,23 +1221,18 @@ __device__ __forceinline__ void flush_hist(Shared6 &sh, const VerifyArgs &a, int
 }
 
 // UNROLL: every unrolled candidate of the three class tables is <= p_max.
-template <bool DUMP, bool UNROLL>
 // __grid_constant__: the cold out-of-line paths take `a` by reference; without it
 // the whole parameter block is copied to the local-memory stack and every field
 // read becomes a local load (long-scoreboard stalls in the hot loop).
-#ifdef GB_NO_GRIDCONST
-#define GB_PARAM VerifyArgs a
-#else
-#define GB_PARAM const __grid_constant__ VerifyArgs a
-#endif
-__global__ void __launch_bounds__(kThreads) verify_kernel(GB_PARAM)
+template <bool DUMP, bool UNROLL>
+__global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant__ VerifyArgs a)
 {
     uint32_t *win = g_win;                     // slot windows (class A | class B) | queues
     __shared__ Shared6 sh;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t halo = a.halo;
     const uint32_t nw_max = halo + a.tile_words + kWinSlack;
-    if (tid == 0) sh.q_base = kSlots * 2 * nw_max;
+    if (tid == 0) sh.q_base = 2 * nw_max;
     for (int i = tid; i < kHistSmem; i += kThreads) sh.hist[i] = 0;
     for (int i = tid; i < 3 * kK; i += kThreads) (&sh.histc[0][0])[i] = 0;
     Acc acc;
@@ -1426,52 +1251,6 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(GB_PARAM)
     uint32_t ns_run = 0;                       // thread 0: running steady count (monotone)
     const MedSched med{a.med_idx, a.med_off};
 
-#if GB_WS
-    // Warp-specialized pipeline: at step s the sieving warps (0 .. kSieveWarps-1)
-    // build tile s in slot s%2 while the marking warps consume tile s-1 from the
-    // other slot; one CTA barrier per step.
-    constexpr int kNS = 32 * kSieveWarps;
-    const bool sieving = warp < kSieveWarps;
-    const uint64_t n_my = t_end - t_begin;
-    for (uint64_t st = 0; st <= n_my; ++st) {
-        if (sieving) {
-            if (st < n_my) {
-                const int slot = (int)(st & 1);
-                const uint64_t u0 = a.u_first + (t_begin + st) * a.tile_words;
-                const uint32_t tw = (uint32_t)min((uint64_t)a.tile_words, a.u_end - u0);
-                const int64_t g0 = (int64_t)u0 - (int64_t)halo;
-                uint32_t *wA = win + slot * 2 * nw_max, *wB = wA + nw_max;
-                if (tid == 0) {
-                    sh.ns[slot] = steady_count(cy, g0, a.sp, ns_run);
-                    sh.next_round[slot] = 0;
-                }
-                group_sync<kNS>();
-                cy.n_steady = sh.ns[slot] & 0x7FFFFFFFu;
-                cy.init = sh.ns[slot] >> 31;
-                if (cy.tile_m == kTileM)
-                    sieve6_window<true, kNS>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask,
-                                             a.lmask_g0, a.lmask_stride, tid);
-                else
-                    sieve6_window<false, kNS>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask,
-                                              a.lmask_g0, a.lmask_stride, tid);
-                cy.have_prev = true;
-            }
-        } else if (st >= 1) {
-            const int slot = (int)((st - 1) & 1);
-            const uint64_t u0 = a.u_first + (t_begin + st - 1) * a.tile_words;
-            const uint32_t tw = (uint32_t)min((uint64_t)a.tile_words, a.u_end - u0);
-            const uint32_t *wA = win + slot * 2 * nw_max, *wB = wA + nw_max;
-            mark_tile<DUMP, UNROLL>(sh, sh.next_round[slot], u0, tw, wA, wB, halo, a, acc, best_p, lane,
-                                    warp - kSieveWarps);
-        }
-        __syncthreads();
-        // periodic flush of the shared histograms keeps their 32-bit bins exact
-        if ((st & 63) == 63 || st == n_my) {
-            flush_hist(sh, a, tid);
-            __syncthreads();
-        }
-    }
-#else
     for (uint64_t tile = t_begin; tile < t_end; ++tile) {
         const uint64_t u0 = a.u_first + tile * a.tile_words;
         const uint32_t tw = (uint32_t)min((uint64_t)a.tile_words, a.u_end - u0);
@@ -1486,11 +1265,11 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(GB_PARAM)
         cy.n_steady = sh.ns[0] & 0x7FFFFFFFu;
         cy.init = sh.ns[0] >> 31;
         if (cy.tile_m == kTileM)
-            sieve6_window<true, kThreads>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask,
-                                          a.lmask_g0, a.lmask_stride, tid);
+            sieve6_window<true>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask, a.lmask_g0,
+                                a.lmask_stride, tid);
         else
-            sieve6_window<false, kThreads>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask,
-                                           a.lmask_g0, a.lmask_stride, tid);
+            sieve6_window<false>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask, a.lmask_g0,
+                                 a.lmask_stride, tid);
         cy.have_prev = true;
         __syncthreads();
         mark_tile<DUMP, UNROLL>(sh, sh.next_round[0], u0, tw, wA, wB, halo, a, acc, best_p, lane, warp);
@@ -1498,7 +1277,6 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(GB_PARAM)
         __syncthreads();
         flush_hist(sh, a, tid);
     }
-#endif
     acc.verified = acc.evens - acc.unres;
 
     flush_acc(acc, a.result, lane);
@@ -1519,22 +1297,7 @@ __global__ void __launch_bounds__(kThreads) sieve_out_kernel(const __grid_consta
     uint32_t *wA = win, *wB = win + nw_max;
     __shared__ uint32_t spread3[256];          // bit j of a byte -> bit 3j
     __shared__ uint32_t sh_ns;
-    __shared__ __align__(8) uint64_t stage_bar[kStageBufs];
-    __shared__ uint32_t stage_done[kStageBufs];
     const int tid = threadIdx.x;
-    // TMA staging ring of base-prime tiles after the two windows (16 B aligned)
-    TmaStage stg;
-    stg.buf = (uint4 *)(win + ((2 * nw_max + 3) & ~3u));
-    stg.bar = stage_bar;
-    stg.done = stage_done;
-    for (uint32_t b = 0; b < kStageBufs; ++b) stg.uses[b] = 0;
-    if (tid == 0) {
-        for (uint32_t b = 0; b < kStageBufs; ++b) {
-            mbar_init(stage_bar + b, 1);
-            stage_done[b] = 0;
-        }
-        mbar_fence_init();
-    }
     for (int i = tid; i < 256; i += kThreads) {
         uint32_t v = 0;
         for (int j = 0; j < 8; ++j) v |= ((i >> j) & 1u) << (3 * j);
@@ -1560,13 +1323,11 @@ __global__ void __launch_bounds__(kThreads) sieve_out_kernel(const __grid_consta
         cy.n_steady = sh_ns & 0x7FFFFFFFu;
         cy.init = sh_ns >> 31;
         if (cy.tile_m == kTileM)
-            sieve6_window<true, kThreads, kSieveStaged>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy,
-                                                MedSched{a.med_idx, a.med_off}, a.i_b2, a.i_b1, a.lmask,
-                                                a.lmask_g0, a.lmask_stride, tid, &stg);
+            sieve6_window<true>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
+                                a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride, tid);
         else
-            sieve6_window<false, kThreads, kSieveStaged>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy,
-                                                 MedSched{a.med_idx, a.med_off}, a.i_b2, a.i_b1, a.lmask,
-                                                 a.lmask_g0, a.lmask_stride, tid, &stg);
+            sieve6_window<false>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
+                                 a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride, tid);
         cy.have_prev = true;
         __syncthreads();
         for (uint32_t i = tid; i < tw; i += kThreads) {
@@ -1592,29 +1353,25 @@ __global__ void __launch_bounds__(kThreads) sieve_out_kernel(const __grid_consta
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-cudaError_t configure_verify(size_t smem_max)
+// Dynamic shared memory opt-in, once per device, at the largest size these kernels
+// are ever launched with (kVerifySmemMax / kSieveOutSmemMax, gb_internal.h).
+cudaError_t configure_verify()
 {
-    const int sm = (int)smem_max;
-    cudaError_t e = cudaFuncSetAttribute(verify_kernel<false, false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(verify_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(verify_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(verify_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    static std::atomic<uint64_t> d0{0}, d1{0}, d2{0}, d3{0};
+    constexpr int sm = (int)kVerifySmemMax;
+    cudaError_t e = ensure_dyn_smem((const void *)verify_kernel<false, false>, sm, d0);
+    if (e == cudaSuccess) e = ensure_dyn_smem((const void *)verify_kernel<true, false>, sm, d1);
+    if (e == cudaSuccess) e = ensure_dyn_smem((const void *)verify_kernel<false, true>, sm, d2);
+    if (e == cudaSuccess) e = ensure_dyn_smem((const void *)verify_kernel<true, true>, sm, d3);
     return e;
 }
 
 cudaError_t launch_sieve_out(const SieveOutArgs &a, int grid, size_t smem, cudaStream_t st)
 {
-    static size_t configured = 0;
-    if (smem > configured) {
-        const cudaError_t e = cudaFuncSetAttribute(sieve_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = smem;
-    }
+    static std::atomic<uint64_t> done{0};
+    if (smem > kSieveOutSmemMax) return cudaErrorInvalidValue;
+    const cudaError_t e = ensure_dyn_smem((const void *)sieve_out_kernel, (int)kSieveOutSmemMax, done);
+    if (e != cudaSuccess) return e;
     sieve_out_kernel<<<grid, kThreads, smem, st>>>(a);
     count_launch();
     return cudaGetLastError();
@@ -1623,6 +1380,7 @@ cudaError_t launch_sieve_out(const SieveOutArgs &a, int grid, size_t smem, cudaS
 int verify_blocks_per_sm(size_t smem)
 {
     int nb = 0;
+    if (configure_verify() != cudaSuccess) return 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, verify_kernel<false, true>, kThreads, smem) !=
         cudaSuccess)
         return 1;
@@ -1631,6 +1389,9 @@ int verify_blocks_per_sm(size_t smem)
 
 cudaError_t launch_verify(const VerifyArgs &a, int grid, size_t smem, cudaStream_t st)
 {
+    if (smem > kVerifySmemMax) return cudaErrorInvalidValue;
+    const cudaError_t e = configure_verify();
+    if (e != cudaSuccess) return e;
     const bool unroll = a.p_fallback - 2 >= kUnrollPMax;   // p_fallback = largest candidate + 2
     if (a.dump) {
         if (unroll) verify_kernel<true, true><<<grid, kThreads, smem, st>>>(a);

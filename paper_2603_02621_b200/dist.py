@@ -44,7 +44,7 @@ def reduce_result(result: torch.Tensor, group=None) -> None:
         return
     s1 = result[gb.R_EVENS:gb.R_CHK_HI32 + 1]            # SUM fields 1..7
     s2 = result[gb.R_HIST:gb.R_HIST + gb.NBINS]          # SUM hist
-    mx = result[gb.R_MAX_KEY:gb.R_MAX_KEY + 1]
+    mx = torch.stack([result[gb.R_MAX_KEY], result[gb.R_MAX_PMIN_RAW]])
     mn = result[gb.R_FIRST_UNRESOLVED_N:gb.R_FIRST_UNRESOLVED_N + 1]
     sums = torch.cat([s1, s2])
     dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
@@ -53,6 +53,7 @@ def reduce_result(result: torch.Tensor, group=None) -> None:
     result[gb.R_EVENS:gb.R_CHK_HI32 + 1] = sums[:s1.numel()]
     result[gb.R_HIST:gb.R_HIST + gb.NBINS] = sums[s1.numel():]
     result[gb.R_MAX_KEY] = mx[0]
+    result[gb.R_MAX_PMIN_RAW] = mx[1]
     result[gb.R_FIRST_UNRESOLVED_N] = mn[0]
 
 

@@ -37,10 +37,12 @@ R_CHK_HI32 = _c_int(_defs["GB_R_CHK_HI32"])
 R_FIRST_UNRESOLVED_N = _c_int(_defs["GB_R_FIRST_UNRESOLVED_N"])
 R_MAX_KEY = _c_int(_defs["GB_R_MAX_KEY"])
 R_CHK_RAW = _c_int(_defs["GB_R_CHK_RAW"])
+R_MAX_PMIN_RAW = _c_int(_defs["GB_R_MAX_PMIN_RAW"])
 R_HIST = _c_int(_defs["GB_R_HIST"])
 NBINS = _c_int(_defs["GB_NBINS"])
 RESULT_WORDS = R_HIST + NBINS
 KEY_SHIFT = _c_int(_defs["GB_KEY_SHIFT"])
+KEY_PMAX = _c_int(_defs["GB_KEY_PMAX"])
 PMAX_LIMIT = _c_int(_defs["GB_PMAX_LIMIT"])
 RESULT_VERSION = _c_int(_defs["GB_RESULT_VERSION"])
 U64_MAX = (1 << 64) - 1
@@ -193,7 +195,11 @@ def _ptr_stream(stream) -> int | None:
 
 # ---- result decoding (host side, plain integer bookkeeping) ------------------
 def decode_result(words, origin: int = 0) -> dict:
-    """Decode a finalized GB_RESULT_WORDS int64 vector into named fields."""
+    """Decode a finalized GB_RESULT_WORDS int64 vector into named fields.
+    chk192 = sum p_min(n) * floor(n/192) mod 2^64 (the block checksum the kernels
+    accumulate; the exact sum n * p_min comes from a per-n dump).  If some p_min
+    reached GB_KEY_PMAX the key's p field saturates: max_pmin is then the raw
+    maximum and max_pmin_n is -1 (unknown)."""
     w = [int(x) for x in (words.tolist() if hasattr(words, "tolist") else words)]
     if w[R_VERSION] != RESULT_VERSION:
         raise ValueError("result vector has a bad version word (not initialised?)")
@@ -205,11 +211,13 @@ def decode_result(words, origin: int = 0) -> dict:
         max_p, max_n = p, origin + 2 * idx
     else:
         max_p, max_n = 0, 0
+    if w[R_MAX_PMIN_RAW] > max_p:
+        max_p, max_n = w[R_MAX_PMIN_RAW], -1
     out = {
         "evens": w[R_EVENS], "verified": w[R_VERIFIED],
         "fastpath_unresolved": w[R_FASTPATH_UNRESOLVED], "unresolved": w[R_UNRESOLVED],
         "first_unresolved_n": w[R_FIRST_UNRESOLVED_N], "max_pmin": max_p, "max_pmin_n": max_n,
-        "sum_pmin": w[R_SUM_PMIN], "chk": chk,
+        "sum_pmin": w[R_SUM_PMIN], "chk192": chk,
     }
     out["hist"] = w[R_HIST:R_HIST + NBINS]
     return out

@@ -77,8 +77,8 @@ def to_words(r, gb):
     w[gb.R_FASTPATH_UNRESOLVED] = r["fastpath_unresolved"]
     w[gb.R_UNRESOLVED] = r["unresolved"]
     w[gb.R_SUM_PMIN] = r["sum_pmin"]
-    w[gb.R_CHK_LO32] = r["chk"] & 0xFFFFFFFF
-    w[gb.R_CHK_HI32] = r["chk"] >> 32
+    w[gb.R_CHK_LO32] = r["chk192"] & 0xFFFFFFFF
+    w[gb.R_CHK_HI32] = r["chk192"] >> 32
     w[gb.R_FIRST_UNRESOLVED_N] = r["first_unresolved_n"]
     if r["max_pmin"]:
         w[gb.R_MAX_KEY] = (r["max_pmin"] << gb.KEY_SHIFT) | ((1 << gb.KEY_SHIFT) - 1 - r["max_pmin_n"] // 2)
@@ -90,7 +90,7 @@ def test_decode_roundtrip():
     from paper_2603_02621_b200 import gb
     r, _ = oracle.verify(4, 200001)
     d = gb.decode_result(to_words(r, gb))
-    for k in oracle.FIELDS:
+    for k in oracle.AGG_FIELDS:
         assert d[k] == r[k], k
     assert d["hist"] == r["hist"].tolist()
 
@@ -139,6 +139,6 @@ def test_gloo_reduce_matches_full_range(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     want, _ = oracle.verify(lo, hi, p_fast=7)
-    for k in oracle.FIELDS:
+    for k in oracle.AGG_FIELDS:
         assert got[k] == want[k], k
     assert got["hist"] == want["hist"].tolist()

@@ -27,7 +27,7 @@ def test_resident_1e6_dump_vs_oracle(V):
     got, d = V.run_resident(4, 10**6 + 1, bits, dump=True)
     want, wd = oracle.verify(4, 10**6 + 1, p_fast=65521, dump=True)
     assert np.array_equal(d.cpu().numpy().astype(np.uint32), wd)
-    for k in oracle.FIELDS:
+    for k in oracle.AGG_FIELDS:
         assert got[k] == want[k], k
 
 
@@ -36,7 +36,7 @@ def test_resident_1e9_vs_golden(V):
     bits = V.sieve_segment(0, (10**9 + 1 - 3) // 128 + 1)
     got, _ = V.run_resident(4, 10**9 + 1, bits)
     g = json.load(open(os.path.join(GOLDEN, "verify_1e09.json")))["result"]
-    for k in oracle.FIELDS:
+    for k in oracle.AGG_FIELDS:
         assert got[k] == g[k], k
     hist = np.zeros(oracle.NBINS, np.int64)
     for i, c in g["hist"].items():

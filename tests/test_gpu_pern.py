@@ -22,7 +22,7 @@ def V():
 
 
 def same(got, want, what):
-    for k in oracle.FIELDS:
+    for k in oracle.AGG_FIELDS:
         assert got[k] == want[k], (what, k, got[k], want[k])
     assert np.array_equal(np.asarray(got["hist"], dtype=np.int64), np.asarray(want["hist"], dtype=np.int64)), what
 

@@ -29,7 +29,7 @@ def test_top_of_u64_window_vs_oracle(V):
     got, d = V.run(LO, HI, dump=True)
     want, wd = oracle.verify(LO, HI, p_fast=65521, dump=True)
     assert np.array_equal(d.cpu().numpy().astype(np.uint32), wd)
-    for k in oracle.FIELDS:
+    for k in oracle.AGG_FIELDS:
         assert got[k] == want[k], (k, got[k], want[k])
     assert np.array_equal(np.asarray(got["hist"], dtype=np.int64), want["hist"])
     # the per-n kernel and single_check agree at the very top
