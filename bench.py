@@ -1,15 +1,20 @@
 #!/usr/bin/env python3
-"""Benchmark: exhaustive minimal-Goldbach-prime verification of every even n in
-[4, N] (default N = 1e12, BASELINE.json configs[3], the metric's workload) on
-1..8 B200s.  One "step" = the whole hot path over the whole range: K-SIEVE +
+"""Benchmark: exhaustive minimal-Goldbach-prime verification of every even n in a
+range on 1..8 B200s.  Default: [4, 1e12] (BASELINE.json configs[3], the metric's
+workload).  One "step" = the whole hot path over the whole range: K-SIEVE +
 inverted marking + fallback in the fused kernel for every strip, the result
 finalize, and the NCCL reduction of the result vector.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--N 1e12] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1|c2|c3|c4|c5]
+                  [--N 1e13] [--mode bulk|pern|resident] [--impl ours|reference]
 
 Prints ONE JSON line on rank 0.  Metric: even n verified per second, whole job,
 device-timed (CUDA events on the launching stream, max over ranks), L2 flushed
-between steps.  Strong scaling: the range is fixed and sharded over ranks.
+between steps.  Strong scaling: the range is fixed and sharded over ranks.  The
+line carries the result of the last step and the verdict of checking it against
+the oracle-written golden of that range (tests/golden/verify_<tag>.json) when one
+exists, else against the invariants every run must satisfy (unresolved == 0,
+sum of the histogram == evens); the process exits 1 if that check fails.
 `--impl reference` times the CPU oracle (oracle/, the paper's cpu_goldbach
 definition) on the host cores on a bounded sample of the same
 workload -- the reference arm of this tier.
@@ -18,6 +23,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -28,8 +34,19 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "even n verified/sec (whole box, device-timed) to N=1e12"
+BASELINE_METRIC = "even n verified/sec (whole box, device-timed) to N=1e12 at 1/2/4/8 B200; sieve GB/s"
 UNIT = "even_n/s"
+NSM = 148
+
+# BASELINE.json configs: (lo, hi, origin, golden tag, description)
+TOP = 4 * 10**18
+WORKLOADS = {
+    "c1": (4, 10**6 + 1, 0, "1e06", "C1: every even n in [4, 1e6]"),
+    "c2": (4, 10**9 + 1, 0, "1e09", "C2: every even n in [4, 1e9]"),
+    "c3": (4, 10**11 + 1, 0, "1e11", "C3: every even n in [4, 1e11]"),
+    "c4": (4, 10**12 + 1, 0, "1e12", "C4: every even n in [4, 1e12]"),
+    "c5": (TOP - 10**11, TOP, TOP - 10**11, "c5_4e18", "C5: every even n in the window [4e18 - 1e11, 4e18)"),
+}
 
 
 def parse():
@@ -37,26 +54,41 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--N", type=float, default=1e12)
-    ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
-                    help="c4: every even n in [4, N] (the metric's workload); c5: the window "
-                         "[4e18 - 1e11, 4e18) of BASELINE.json configs[4]")
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--N", type=float, default=None, help="custom range [4, N] (overrides --workload)")
     ap.add_argument("--p-max", type=int, default=65521)
     ap.add_argument("--mode", default="bulk", choices=["bulk", "pern", "resident"],
                     help="bulk: the product path (inverted bulk marking); pern: the paper's per-n "
                          "gpu3 kernel (NEXT-1, PAPER.md:82-95); resident: the paper's gpu2 with the "
                          "whole odd bitset of [3, hi) sieved into HBM each step (NEXT-2, PAPER.md:41-59)")
     ap.add_argument("--strips-per-rank", type=int, default=None,
-                    help="default 8 for c4 (balances the growth of work with n), 2 for c5 (the "
-                         "window's cost is flat; fewer partial K-LARGE chunks)")
+                    help="default 8 (balances the growth of work with n); 2 for c5 (the window's cost "
+                         "is flat; fewer partial K-LARGE chunks)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sieve", action="store_true", help="skip the standalone sieve GB/s leg")
+    ap.add_argument("--no-check", action="store_true", help="do not exit 1 on a failed result check")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     a = ap.parse_args()
     if a.strips_per_rank is None:
-        a.strips_per_rank = 2 if a.workload == "c5" else 8
+        a.strips_per_rank = 2 if a.workload == "c5" and a.N is None else 8
     return a
+
+
+def workload(args):
+    """(lo, hi, origin, golden tag or None, description)"""
+    if args.N is not None:
+        N = int(args.N)
+        return 4, N + 1, 0, f"{N:.0e}".replace("+", ""), f"every even n in [4, {N:.0e}]"
+    return WORKLOADS[args.workload]
+
+
+def metric_name(args):
+    if args.N is None and args.workload == "c4" and args.mode == "bulk":
+        return BASELINE_METRIC
+    _, _, _, _, desc = workload(args)
+    return f"even n verified/sec (whole box, device-timed), {desc}" + (
+        f" [{args.mode} mode]" if args.mode != "bulk" else "")
 
 
 # ----------------------------------------------------------------- clocks
@@ -101,21 +133,12 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- CPU oracle legs
-def workload(args):
-    """(lo, hi, origin, description, algorithmic int32 ops per even n) of the run."""
-    if args.workload == "c5":
-        top = 4 * 10**18
-        return top - 10**11, top, top - 10**11, "C5 window: every even n in [4e18 - 1e11, 4e18)", C5_OPS_PER_EVEN
-    N = int(args.N)
-    return 4, N + 1, 0, f"N={N:.0e} exhaustive verification, even n in [4, N]", ALU_OPS_PER_EVEN
-
-
 def oracle_sample(hi: int, target_s: float, lo_min: int = 4):
     """Time the CPU oracle (as it stands) on a top slice of [lo_min, hi), growing the
     slice until it has run for at least target_s seconds."""
     from oracle import oracle
     threads = oracle.default_threads()
-    span = 1 << 27
+    span = 1 << 22
     while True:
         lo = max(lo_min, hi - span)
         t0 = time.perf_counter()
@@ -131,19 +154,18 @@ def oracle_sample(hi: int, target_s: float, lo_min: int = 4):
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
-    lo, hi, _, desc, _ = workload(args)
+    lo, hi, _, _, desc = workload(args)
     per_step = max(1.0, args.cpu_seconds / 4)
     for _ in range(args.warmup):
         oracle_sample(hi, per_step / 4, lo)
-    vals, times, evens = [], [], 0
+    times, evens = [], 0
     first = oracle_sample(hi, per_step, lo)
     for i in range(args.steps):
         s = first if i == 0 else oracle_sample(hi, per_step, lo)
-        vals.append(s["value"])
         times.append(s["seconds"])
         evens += s["evens"]
     value = evens / sum(times)
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    line = {"metric": metric_name(args), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (deterministic number-theoretic range)", "impl": "reference",
@@ -152,6 +174,97 @@ def run_reference(args, rank: int, world: int):
                              "sample": f"{args.steps} top-of-range slices of [{lo}, {hi}), ~{per_step:.1f} s each"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- roofline yardsticks
+def small_primes(limit: int):
+    import numpy as np
+    s = np.ones(limit + 1, dtype=bool)
+    s[:2] = False
+    for i in range(2, int(limit**0.5) + 1):
+        if s[i]:
+            s[i * i::i] = False
+    return np.flatnonzero(s)
+
+
+def recip_sum(a: int, b: int) -> float:
+    """sum of 1/p over primes a < p <= b: exact to 1e7, Mertens' ln ln x beyond
+    (the difference of two ln ln terms is accurate to ~1e-6 there)."""
+    import numpy as np
+    cut = 10**7
+    ps = small_primes(min(b, cut))
+    s = float(np.sum(1.0 / ps[(ps > a) & (ps <= b)]))
+    if b > cut:
+        s += math.log(math.log(b)) - math.log(math.log(max(a, cut)))
+    return s
+
+
+def mark_word_iters(hi: int) -> float:
+    """SURVEY.md 8(d) "Algorithmic work per even n": 64-bit word-iterations per even
+    n of the inverted loop with 64-even exit (the table's values at its N, log-linear
+    in log10 N between them)."""
+    pts = [(9, 0.74), (11, 0.92), (12, 1.01), (18.6, 1.63)]
+    x = math.log10(hi)
+    if x <= pts[0][0]:
+        return pts[0][1]
+    for (x0, y0), (x1, y1) in zip(pts, pts[1:]):
+        if x <= x1:
+            return y0 + (y1 - y0) * (x - x0) / (x1 - x0)
+    return pts[-1][1]
+
+
+def load_peaks():
+    """MEASURED_PEAKS.json (driver) + profiles/peaks_int.json (scripts/micro/peaks_int.cu
+    on a B200 of this pool); returns the per-SM lane rates and the SM clock."""
+    peaks, pint = {}, None
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    try:
+        pint = json.load(open(os.path.join(ROOT, "profiles", "peaks_int.json")))
+    except Exception:
+        pass
+    return peaks, pint
+
+
+def ncu_traffic(kernel: str, tag: str, mode: str):
+    """DRAM read+write bytes per even n of `kernel` from the committed ncu --set full
+    capture of this workload (profiles/*_<kernel>_<tag>[_<mode>]_ncu.json), or None."""
+    import glob
+    suffix = f"_{tag}" + ("" if mode == "bulk" else f"_{mode}")
+    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_{kernel}{suffix}_ncu.json")))
+    if not caps:
+        return None, None
+    cap = json.load(open(caps[-1]))
+    return cap.get("dram_bytes_per_even"), os.path.relpath(caps[-1], ROOT)
+
+
+# ----------------------------------------------------------------- result check
+def check_result(res, lo, hi, tag):
+    """Compare with the oracle golden of this range if one exists, else check the
+    invariants.  Returns (ok, what)."""
+    from oracle import oracle
+    from oracle.oracle import AGG_FIELDS, NBINS
+    evens = oracle.n_evens(lo, hi)
+    inv = (res["evens"] == evens and res["verified"] == evens and res["unresolved"] == 0
+           and sum(res["hist"]) == evens)
+    path = os.path.join(ROOT, "tests", "golden", f"verify_{tag}.json") if tag else None
+    if path and os.path.exists(path):
+        g = json.load(open(path))
+        if (g["lo"], g["hi"]) == (lo, hi) and "chk192" in g["result"]:
+            gr = g["result"]
+            bad = [k for k in AGG_FIELDS if res[k] != gr[k]]
+            hist = [0] * NBINS
+            for i, c in gr["hist"].items():
+                hist[int(i)] = c
+            if list(res["hist"]) != hist:
+                bad.append("hist")
+            return inv and not bad, {"golden": os.path.relpath(path, ROOT), "mismatch": bad,
+                                     "invariants": inv}
+    return inv, {"golden": None, "invariants": inv,
+                 "note": "no oracle golden for this range: invariants only (evens, all verified, "
+                         "no unresolved, sum hist = evens)"}
 
 
 # ----------------------------------------------------------------- GPU arm
@@ -164,6 +277,7 @@ def main():
         run_reference(args, rank, world)
         return
 
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -185,37 +299,40 @@ def main():
     from paper_2603_02621_b200 import dist as gdist
     from paper_2603_02621_b200.verifier import Verifier
 
-    lo, hi, origin, desc, ops_per_even = workload(args)
+    lo, hi, origin, tag, desc = workload(args)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-    V = Verifier(hi_max=hi, p_max=args.p_max, origin=origin, device=local, stream=stream)
+    n_bits_words = (hi - 3) // 128 + 1 if args.mode == "resident" else 0
+    # resident mode sieves every word of [3, hi): the context must cover their top q
+    hi_max = max(hi, 3 + 128 * n_bits_words) if n_bits_words else hi
+    V = Verifier(hi_max=hi_max, p_max=args.p_max, origin=origin, device=local, stream=stream)
     strips = gdist.rank_strips(gdist.plan_strips(lo, hi, args.strips_per_rank * world), rank, world)
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(4 * l2_bytes, 1 << 28) // 4, dtype=torch.int32, device=dev)
-
-    bits = None
-    if args.mode == "resident":
-        n_bits_words = (hi - 3) // 128 + 1
-        bits = torch.empty(n_bits_words, dtype=torch.int64, device=dev)
+    bits = torch.empty(n_bits_words, dtype=torch.int64, device=dev) if n_bits_words else None
 
     def step(k_events=None):
         r = V.new_result()
         if bits is not None:                         # gpu2: sieve [3, hi) into HBM, then per-n lookups
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             gb.gb_sieve_segment(V.ctx, 0, bits.numel(), bits, stream)
             for a, b in strips:
                 gb.gb_verify_range_resident(V.ctx, a, b, args.p_max, bits, bits.numel(), r, None, stream)
-            V.finalize(r)
-            gdist.reduce_result(r)
-            return r
-        for a, b in strips:
+            e1.record(stream)
             if k_events is not None:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-            V.verify(a, b, r, p_max=args.p_max, mode=args.mode)
-            if k_events is not None:
-                e1.record(stream)
                 k_events.append((e0, e1))
+        else:
+            for a, b in strips:
+                if k_events is not None:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                V.verify(a, b, r, p_max=args.p_max, mode=args.mode)
+                if k_events is not None:
+                    e1.record(stream)
+                    k_events.append((e0, e1))
         V.finalize(r)
         gdist.reduce_result(r)
         return r
@@ -227,7 +344,7 @@ def main():
     sampler = ClockSampler(local)
     sampler.start()
     launches0 = gb.gb_launch_count()
-    step_ms, k_events, results = [], [], []
+    k_events, results = [], []
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -243,6 +360,7 @@ def main():
     if world > 1:
         dist.barrier()
     launches = gb.gb_launch_count() - launches0
+    launches_per_step = launches / args.steps
     if world > 1:                                    # whole job: every rank's launches
         lt = torch.tensor([launches], dtype=torch.int64, device=dev)
         dist.all_reduce(lt, op=dist.ReduceOp.SUM)
@@ -259,9 +377,7 @@ def main():
     evens = res["evens"]
     value = evens * args.steps / (box_ms / 1e3)
 
-    # ---- end to end through the C-ABI host entry point (host result buffer)
-    e2e = None
-    import numpy as np
+    # ---- end to end through the public API with host buffers
     h_res = torch.empty(gb.RESULT_WORDS, dtype=torch.int64).pin_memory()
     e2e_steps = max(1, min(args.steps, 3))
     if world > 1:
@@ -269,10 +385,15 @@ def main():
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        acc = np.zeros(gb.RESULT_WORDS, dtype=np.int64)
-        for a, b in strips:
-            gb.gb_verify_range_host(V.ctx, a, b, args.p_max, h_res, None, stream)
-            acc += h_res.numpy()
+        if args.mode == "bulk":                      # the C-ABI host entry: init + verify + finalize + D2H
+            acc = np.zeros(gb.RESULT_WORDS, dtype=np.int64)
+            for a, b in strips:
+                gb.gb_verify_range_host(V.ctx, a, b, args.p_max, h_res, None, stream)
+                acc += h_res.numpy()
+        else:                                        # Verifier API of the comparison modes + D2H
+            r = step()
+            h_res.copy_(r, non_blocking=True)
+            stream.synchronize()
     if world > 1:
         tt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -280,49 +401,70 @@ def main():
     else:
         e2e_s = time.perf_counter() - t0
     e2e = {"value": evens * e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0,
-           "d2h_bytes_per_step": 8 * gb.RESULT_WORDS * len(strips),
-           "note": "gb_verify_range_host per strip: init+verify+finalize+D2H of the 52 KB result; "
-                   "inputs are (lo, hi, p_max) scalars, no array H2D; cross-rank sum not included"}
+           "d2h_bytes_per_step": 8 * gb.RESULT_WORDS * (len(strips) if args.mode == "bulk" else 1),
+           "note": ("gb_verify_range_host per strip (C ABI, host result buffer): init + verify + finalize + "
+                    "D2H of the 52 KB result; the inputs are (lo, hi, p_max) scalars, so no array H2D"
+                    if args.mode == "bulk" else
+                    f"Verifier API ({args.mode} mode) + D2H of the 52 KB result; scalar inputs")}
 
-    # ---- roofline of the dominant kernel (the fused verify kernel)
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
+    # ---- rooflines
+    peaks, pint = load_peaks()
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    hbm = peaks.get("hbm_gbs") or 6545.9
+    if pint:
+        rates = pint["per_sm_lane_ops_per_clk"]
+        alu_rate, red_rate = rates["lop3"], rates["red_shared_and"]
+        peak_src = "profiles/peaks_int.json (scripts/micro/peaks_int.cu, measured on a B200 of this pool)"
+    else:
+        alu_rate, red_rate = 64.0, 16.0
+        peak_src = "nominal (profiles/peaks_int.json absent): 64 ALU / 16 shared-RED lanes per clk per SM"
+    alu_peak = NSM * alu_rate * sm_mhz * 1e6 / 1e12          # T int32 lane-ops/s
+    red_peak = NSM * red_rate * sm_mhz * 1e6 / 1e12
     n_launch = len(kern_ms)
     avg_launch_s = (sum(kern_ms) / n_launch) / 1e3 if n_launch else float("nan")
-    evens_per_launch = evens / max(1, len(strips) * world)
-    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
-    alu_peak = 148 * 64 * sm_mhz * 1e6 / 1e12           # T int32 lane-ops/s on the ALU pipe
-    achieved = ops_per_even * evens_per_launch / avg_launch_s / 1e12 if n_launch else None
-    traffic, traffic_src = None, None
-    try:   # DRAM bytes per even n of verify_kernel from the latest committed ncu --set full capture
-        import glob
-        caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_verify_kernel_ncu.json")))
-        if caps:
-            cap = json.load(open(caps[-1]))
-            traffic = cap["dram_bytes_per_even"] * evens_per_launch
-            traffic_src = os.path.relpath(caps[-1], ROOT)
-    except Exception:
-        pass
-    roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Tops/s",
-                "frac": achieved / alu_peak if achieved else None, "traffic": traffic,
-                "traffic_note": (f"DRAM read+write bytes per launch, scaled per even n from {traffic_src}"
-                                 if traffic_src else None),
-                "kernel": "verify_kernel (fused sieve + mark + fallback)",
-                "ops_per_even": ops_per_even,
-                "peak_basis": f"148 SM x 64 int32 lanes/clk (ALU pipe) x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
-                "kernel_ms_per_launch": avg_launch_s * 1e3 if n_launch else None, "launches_timed": n_launch,
-                "kernel_share_of_step": box_kern_ms / box_ms if box_ms else None}
+    evens_per_launch = evens / max(1, n_launch // args.steps) / world
+    sqrt_hi = math.isqrt(hi - 1)
+    clears = recip_sum(2, sqrt_hi)                 # sieve bit-clears per odd (= per even n)
+    clears_red = recip_sum(61, sqrt_hi)            # the part not done by word patterns (p > 61)
+    w_iters = mark_word_iters(hi)
+    ops_per_even = clears + 6 * w_iters            # 1 op per clear, 6 per 64-bit word-iteration
+    dram_pe, dram_src = ncu_traffic("verify_kernel" if args.mode == "bulk" else "pern_kernel", tag or "", args.mode)
+    if args.mode == "bulk":
+        achieved = ops_per_even * evens_per_launch / avg_launch_s / 1e12
+        roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Tops/s",
+                    "frac": achieved / alu_peak,
+                    "traffic": dram_pe * evens_per_launch if dram_pe is not None else None,
+                    "traffic_note": (f"DRAM read+write bytes per launch, scaled per even n from {dram_src}"
+                                     if dram_src else "no ncu capture of this workload in profiles/"),
+                    "kernel": "verify_kernel (fused sieve + mark + fallback)",
+                    "ops_per_even": round(ops_per_even, 4),
+                    "ops_basis": (f"SURVEY 8(d): {clears:.3f} sieve bit-clears per odd (primes to isqrt(hi)) + "
+                                  f"6 int32 ops x {w_iters:.3f} 64-bit mark word-iterations per even n"),
+                    "peak_basis": f"148 SM x {alu_rate:.1f} LOP3 lanes/clk x {sm_mhz:.0f} MHz; {peak_src}",
+                    "kernel_ms_per_launch": avg_launch_s * 1e3, "launches_timed": n_launch,
+                    "kernel_share_of_step": box_kern_ms / box_ms if box_ms else None}
+    else:
+        # comparison modes (the paper's own designs): a bitset in HBM written once and read
+        # by per-n lookups -- algorithmic bytes 1 bit written + 1 bit read per even n
+        bytes_pe = 0.25
+        achieved = bytes_pe * evens_per_launch / avg_launch_s / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                    "traffic": dram_pe * evens_per_launch if dram_pe is not None else None,
+                    "kernel": f"{args.mode} mode (sieve to HBM/L2 + per-n lookups)",
+                    "bytes_per_even": bytes_pe, "kernel_ms_per_launch": avg_launch_s * 1e3,
+                    "launches_timed": n_launch}
 
     # ---- sieve GB/s (BASELINE.json metric, second half): standalone gb_sieve_segment
     # (K-SIEVE, the paper's odd-only layout PAPER.md:46-51) writing the bitset of the
-    # top 2^34 integers of the range to HBM; bytes written / device time
+    # top 2^34 integers of the range to HBM; bytes written / device time.  Its roofline
+    # is the shared-memory RED pipe (the bit-clears), not HBM.
     sieve = None
-    if not args.no_sieve:
+    sieve_ms_per_int = None
+    if not args.no_sieve and hi > 1 << 30:
         nwords = 1 << 27                                   # u64 words = 2^34 integers, 1 GiB
         w_hi = (hi - 3) // 128
+        if math.isqrt(3 + 128 * w_hi + 126) > V.R:
+            w_hi -= 1                                      # top word must stay within the base primes
         w_lo = max(0, w_hi - nwords)
         out = torch.empty(w_hi - w_lo, dtype=torch.int64, device=dev)
         for _ in range(2):
@@ -338,46 +480,65 @@ def main():
         torch.cuda.synchronize()
         ms = statistics.median(a.elapsed_time(b) for a, b in ev)
         nbytes = 8 * (w_hi - w_lo)
-        hbm = peaks.get("hbm_gbs") or 6545.9
+        odds = 64 * (w_hi - w_lo)
+        sieve_ms_per_int = ms / (2 * odds)
+        red_achieved = clears_red * odds / (ms / 1e3) / 1e12
         sieve = {"value": nbytes / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_launch": ms,
-                 "odd_integers_per_s": 64 * (w_hi - w_lo) / (ms / 1e3),
+                 "odd_integers_per_s": odds / (ms / 1e3),
                  "window": f"odd q in [{3 + 128 * w_lo}, {3 + 128 * w_hi})",
                  "kernel": "sieve_out_kernel (gb_sieve_segment)",
-                 "hbm_frac": nbytes / (ms / 1e3) / 1e9 / hbm, "hbm_peak_gbps": hbm}
+                 "hbm_frac": nbytes / (ms / 1e3) / 1e9 / hbm, "hbm_peak_gbps": hbm,
+                 "roofline": {"bound": "smem_red", "achieved": red_achieved, "peak": red_peak, "unit": "Tops/s",
+                              "frac": red_achieved / red_peak,
+                              "ops_basis": f"{clears_red:.3f} bit-clears per odd by primes 61 < p <= isqrt(hi) "
+                                           "(SURVEY 8(d) 'excl. p <= 61': the clears no word pattern does)",
+                              "peak_basis": f"148 SM x {red_rate:.2f} red.shared.and lanes/clk x {sm_mhz:.0f} MHz; "
+                                            f"{peak_src}"}}
         del out
+    if args.mode == "bulk" and sieve_ms_per_int is not None:
+        # the fused kernel's two halves: the standalone sieve's time per integer stands
+        # for the fused sieve phase (same sieve6_window code; it also re-interleaves
+        # and writes out, so this over-states the sieve half), the rest is marking
+        span_ints = evens_per_launch * 2
+        t_sieve = sieve_ms_per_int * span_ints / 1e3
+        t_mark = max(avg_launch_s - t_sieve, 1e-12)
+        mark_ach = 6 * w_iters * evens_per_launch / t_mark / 1e12
+        sieve_ach = clears_red * evens_per_launch / t_sieve / 1e12
+        roofline["sieve"] = {"bound": "smem_red", "achieved": sieve_ach, "peak": red_peak, "unit": "Tops/s",
+                             "frac": sieve_ach / red_peak, "est_share_of_kernel": t_sieve / avg_launch_s,
+                             "basis": "standalone gb_sieve_segment time per integer x this launch's integers"}
+        roofline["mark"] = {"bound": "alu", "achieved": mark_ach, "peak": alu_peak, "unit": "Tops/s",
+                            "frac": mark_ach / alu_peak, "est_share_of_kernel": t_mark / avg_launch_s,
+                            "basis": "verify_kernel time minus the sieve estimate; 6 ops x SURVEY word-iterations"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_sample(hi, args.cpu_seconds, lo)
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
+    ok, check = check_result(res, lo, hi, tag) if rank == 0 else (True, None)
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": box_ms / args.steps, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        line = {"metric": metric_name(args), "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": box_ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
                 "data": "synthetic (deterministic number-theoretic range; no dataset)",
-                "config": {"workload": desc, "lo": lo, "hi": hi, "p_max": args.p_max, "strips_per_rank": args.strips_per_rank,
-                           "parallelism": f"range-sharded x{world}", "l2": "flushed between steps",
-                           "mode": args.mode},
-                "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "roofline": roofline,
+                "config": {"workload": desc, "lo": lo, "hi": hi, "p_max": args.p_max,
+                           "strips_per_rank": args.strips_per_rank, "parallelism": f"range-sharded x{world}",
+                           "l2": "flushed between steps", "mode": args.mode},
+                "gpu_launches": launches, "gpu_launches_per_step_per_rank": launches_per_step,
+                "clocks": clocks, "e2e": e2e, "roofline": roofline,
                 "cpu_baseline": cpu, "sieve": sieve,
                 "result": {k: res[k] for k in ("evens", "verified", "fastpath_unresolved", "unresolved",
-                                                  "max_pmin", "max_pmin_n", "sum_pmin", "chk")},
+                                                  "max_pmin", "max_pmin_n", "sum_pmin", "chk192")},
+                "check": dict(check, ok=ok),
                 "step_ms": step_ms}
         print(json.dumps(line), flush=True)
     V.close()
     if world > 1:
         dist.destroy_process_group()
+    if rank == 0 and not ok and not args.no_check:
+        sys.exit(1)
 
-
-# Algorithmic int32 ops per even n at N = 1e12 (SURVEY.md section 8d "Algorithmic
-# work per even n"; derivation in DESIGN.md section "Roofline"):
-#   sieve : 2.387 bit-clears per odd (= per even n), 1 op each
-#   mark  : 1.01 64-bit word-iterations per even n (64-even exit) x 6 int32 ops
-#           (2 funnel shifts, 2 AND, 2 XOR)
-ALU_OPS_PER_EVEN = 2.387 + 1.01 * 6
-# the same yardstick in the C5 window ("4e18 window" row)
-C5_OPS_PER_EVEN = 2.826 + 1.63 * 6
 
 if __name__ == "__main__":
     main()
