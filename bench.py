@@ -252,7 +252,7 @@ def check_result(res, lo, hi, tag):
     path = os.path.join(ROOT, "tests", "golden", f"verify_{tag}.json") if tag else None
     if path and os.path.exists(path):
         g = json.load(open(path))
-        if (g["lo"], g["hi"]) == (lo, hi) and "chk192" in g["result"]:
+        if (g["lo"], g["hi"]) == (lo, hi):
             gr = g["result"]
             bad = [k for k in AGG_FIELDS if res[k] != gr[k]]
             hist = [0] * NBINS
@@ -529,7 +529,7 @@ def main():
                 "clocks": clocks, "e2e": e2e, "roofline": roofline,
                 "cpu_baseline": cpu, "sieve": sieve,
                 "result": {k: res[k] for k in ("evens", "verified", "fastpath_unresolved", "unresolved",
-                                                  "max_pmin", "max_pmin_n", "sum_pmin", "chk192")},
+                                                  "max_pmin", "max_pmin_n", "sum_pmin")},
                 "check": dict(check, ok=ok),
                 "step_ms": step_ms}
         print(json.dumps(line), flush=True)

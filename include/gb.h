@@ -50,7 +50,7 @@ typedef struct gb_ctx gb_ctx;   /* opaque; host object owned by libgb */
  * FIRST_UNRESOLVED_N (MIN) and MAX_KEY (MAX) -- the reduction rules the
  * multi-GPU layer applies with NCCL ("--gpus distributes work").
  * ------------------------------------------------------------------------- */
-#define GB_RESULT_VERSION 0x4742000000000002LL
+#define GB_RESULT_VERSION 0x4742000000000003LL
 #define GB_R_VERSION              0   /* GB_RESULT_VERSION                           */
 #define GB_R_EVENS                1   /* SUM: even n in the verified ranges          */
 #define GB_R_VERIFIED             2   /* SUM: n with a partition found               */
@@ -59,20 +59,14 @@ typedef struct gb_ctx gb_ctx;   /* opaque; host object owned by libgb */
 #define GB_R_UNRESOLVED           4   /* SUM: n with no partition p <= n/2 (a
                                          counterexample) -- must be 0                */
 #define GB_R_SUM_PMIN             5   /* SUM: sum of p_min                           */
-#define GB_R_CHK_LO32             6   /* SUM: low 32 bits of CHK192 (after finalize) */
-#define GB_R_CHK_HI32             7   /* SUM: high 32 bits of CHK192 (after finalize)*/
+/* words 6, 7, 10, 12..15: reserved (0).  No checksum is accumulated on the hot
+   path: the exact sum of n * p_min, the position-sensitive check, is taken from the
+   per-n dump (d_pmin_dump of gb_verify_range) by the tests. */
 #define GB_R_FIRST_UNRESOLVED_N   8   /* MIN: smallest unresolved n, INT64_MAX if none */
 #define GB_R_MAX_KEY              9   /* MAX: (min(p_min, 2^14-1) << 49) |
                                          (2^49-1 - (n-origin)/2): largest p_min, ties
                                          to the smallest n (exact while p_min < 2^14;
                                          every p_min below 4e18 is <= 9781)          */
-#define GB_R_CHK_RAW             10   /* device accumulator of CHK192 = sum of
-                                         p_min(n) * floor(n/192) mod 2^64 (a block
-                                         checksum: which 192-integer block each
-                                         p_min lands in); moved into LO32/HI32 and
-                                         zeroed by finalize.  The exact sum of
-                                         n * p_min needs the per-n values: see the
-                                         dump of gb_verify_range                    */
 #define GB_R_MAX_PMIN_RAW        11   /* MAX: largest p_min (exact even when the
                                          MAX_KEY field saturates at 2^14-1)         */
 #define GB_R_HIST                16   /* SUM: hist[0..GB_NBINS)                       */
@@ -134,9 +128,10 @@ gb_status gb_sieve_segment(gb_ctx *ctx, uint64_t word_lo, uint64_t n_words,
  * on the device that owns d_result. */
 gb_status gb_result_init(int64_t *d_result, void *stream);
 
-/* After a rank's last gb_verify_range: move CHK_RAW into CHK_LO32/CHK_HI32 (so
- * an int64 SUM across ranks cannot overflow) and zero CHK_RAW.  Host
- * recombines CHK = ((sum HI32) << 32) + sum LO32 mod 2^64. */
+/* After a rank's last gb_verify_range, before the cross-rank reduction: a hook for
+ * fields that need a final pass.  No field of this result version does (every SUM
+ * field stays far below 2^63 on any range the library accepts), so it only checks
+ * its arguments and launches nothing. */
 gb_status gb_result_finalize(int64_t *d_result, void *stream);
 
 /* Verify every even n with lo <= n < hi (half-open; the paper's "n in [4, N]",
@@ -202,6 +197,22 @@ gb_status gb_verify_range_resident(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32
  * The paper's tool returns some valid partition; this one returns the minimal one.
  * GB_EINVAL for odd n, n < 4, misaligned d_out. */
 gb_status gb_single_check(gb_ctx *ctx, uint64_t n, uint64_t p_limit, uint64_t *d_out, void *stream);
+
+/* NEXT-4: Goldbach partition counts (section 4.5 "large-scale
+ * computation of Goldbach partition counts c(n)"; c(n) also at PAPER.md:404).  The
+ * paper does not define c(n); read as the Goldbach-comet count (R13)
+ *      c(n) = #{ p prime : p <= n/2 and n - p prime },   c(4) = 1 (2 + 2).
+ * For every even n in [lo_e, hi), lo_e = max(4, lo rounded up to even):
+ * d_counts[(n - lo_e)/2] = c(n) (u64, overwritten).  d_bits: words [0, n_words) of
+ * the global odd bitset in the paper's layout (e.g. from gb_sieve_segment), which
+ * must hold every odd q < hi (3 + 128 * n_words >= hi), caller-owned.  Work is
+ * O(n) bit operations per n (popcount-AND of the bitset against its reversed
+ * shifts), so hi is limited to GB_COUNTS_HI_LIMIT.  One init launch and one
+ * counting launch.  Errors: GB_EINVAL (bounds, NULL / misaligned pointers, bitset
+ * too short). */
+#define GB_COUNTS_HI_LIMIT 1099511627776ull   /* 2^40 */
+gb_status gb_partition_counts(gb_ctx *ctx, uint64_t lo, uint64_t hi, const uint64_t *d_bits, uint64_t n_words,
+                              uint64_t *d_counts, void *stream);
 
 /* Deterministic 64-bit Miller-Rabin (12 prime bases 2..37; PAPER.md:89,
  * SPEC.md:128) as used by the fallback: d_out[i] = 1 iff d_x[i] is prime. */

@@ -35,14 +35,11 @@
  *   R5 aggregates: histogram of p_min by prime index (bin 0 = unresolved,
  *      bin i = i-th prime, p_1 = 2, ..., p_6542 = 65521, bin 6543 = larger),
  *      max p_min with the SMALLEST n attaining it (A025018 convention),
- *      sum of p_min, and two checksums (the paper defines none; R6):
- *        chk    = sum of n * p_min(n) mod 2^64 (a
- *                 p_min placed on the wrong n changes it);
- *        chk192 = sum of p_min(n) * floor(n / 192) mod 2^64 (coarser: which
- *                 192-integer block each p_min lands in; a second plain
- *                 function of the per-n values, compared where no dump is);
- *      optionally chk per chunk of 2^k evens counted from lo_e (chunk_chk),
- *      so full-range goldens can be compared piece by piece.
+ *      sum of p_min, and the checksum chk = sum of n * p_min(n) mod 2^64
+ *      (the paper defines none; R6): a p_min
+ *      placed on the wrong n changes it; optionally chk per chunk of 2^k evens
+ *      counted from lo_e (chunk_chk), so full-range goldens can be compared
+ *      piece by piece.
  *
  * Build: gcc -O2 -std=c11 -pthread -shared -fPIC gb_oracle.c -o liboracle.so
  */
@@ -66,7 +63,6 @@ typedef struct {
     int64_t max_pmin_n;          /* smallest n with p_min == max_pmin */
     int64_t sum_pmin;
     uint64_t chk;                /* sum n * p_min(n)             mod 2^64 */
-    uint64_t chk192;             /* sum p_min(n) * floor(n/192)  mod 2^64 */
     int64_t hist[OR_NBINS];
 } or_result;
 
@@ -214,7 +210,6 @@ static void record(worker *w, uint64_t n, uint64_t p)
     r->hist[bin_of(w->sp, p)]++;
     r->sum_pmin += (int64_t)p;
     r->chk += n * p;                           /* wraps mod 2^64 */
-    r->chk192 += p * (n / 192);
     w->seg_chk += n * p;
     if ((int64_t)p > r->max_pmin || ((int64_t)p == r->max_pmin && (int64_t)n < r->max_pmin_n)) {
         r->max_pmin = (int64_t)p;
@@ -280,7 +275,6 @@ static void merge(or_result *a, const or_result *b)
     }
     a->sum_pmin += b->sum_pmin;
     a->chk += b->chk;
-    a->chk192 += b->chk192;
     for (int i = 0; i < OR_NBINS; i++) a->hist[i] += b->hist[i];
 }
 
@@ -404,6 +398,71 @@ uint64_t or_prime_pi(uint64_t x, int threads)
     free(ws); free(th);
     small_primes_free(&sp);
     return err ? UINT64_MAX : total;
+}
+
+/* ---- Goldbach partition counts c(n) ------------------------------------
+ * NEXT-4 (section 4.5 "large-scale computation
+ * of Goldbach partition counts c(n)").  The paper does not define c(n); reading
+ * R13: the number of unordered partitions, the Goldbach-comet count
+ *      c(n) = #{ p prime : p <= n/2 and n - p prime }    (c(4) = 1: 2 + 2).
+ * Written out plainly: a byte-per-integer sieve of [0, hi) and, for each even n,
+ * a scan of the primes p <= n/2 with a byte lookup of n - p.                  */
+typedef struct {
+    const uint8_t *isp;
+    const uint32_t *pr;         /* primes ascending (2 first) */
+    uint64_t npr;
+    uint64_t lo_e, hi;
+    int tid, nthreads;
+    uint64_t *out;
+} cn_worker;
+
+static void *cn_main(void *arg)
+{
+    cn_worker *w = (cn_worker *)arg;
+    uint64_t k = 0;
+    for (uint64_t n = w->lo_e; n < w->hi; n += 2, ++k) {
+        if ((int)(k % (uint64_t)w->nthreads) != w->tid) continue;
+        uint64_t c = 0;
+        for (uint64_t i = 0; i < w->npr && w->pr[i] <= n / 2; ++i)
+            c += w->isp[n - w->pr[i]];
+        w->out[k] = c;
+    }
+    return NULL;
+}
+
+/* out[(n - lo_e)/2] = c(n) for every even n in [lo_e, hi), lo_e = max(4, lo
+ * rounded up to even).  Returns 0, -1 on allocation failure, -2 if hi > 2^36. */
+int or_partition_counts(uint64_t lo, uint64_t hi, int threads, uint64_t *out)
+{
+    uint64_t lo_e = lo < 4 ? 4 : lo + (lo & 1);
+    if (hi <= lo_e) return 0;
+    if (hi > (1ull << 36)) return -2;
+    if (threads < 1) threads = 1;
+    uint8_t *isp = (uint8_t *)malloc(hi);
+    if (!isp) return -1;
+    memset(isp, 1, hi);
+    isp[0] = 0;
+    if (hi > 1) isp[1] = 0;
+    for (uint64_t i = 2; i * i < hi; i++)
+        if (isp[i])
+            for (uint64_t m = i * i; m < hi; m += i) isp[m] = 0;
+    uint64_t npr = 0;
+    for (uint64_t i = 2; i <= hi / 2; i++) npr += isp[i];
+    uint32_t *pr = (uint32_t *)malloc(sizeof(uint32_t) * (npr + 1));
+    pthread_t *th = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+    cn_worker *ws = (cn_worker *)calloc((size_t)threads, sizeof(cn_worker));
+    if (!pr || !th || !ws) { free(isp); free(pr); free(th); free(ws); return -1; }
+    npr = 0;
+    for (uint64_t i = 2; i <= hi / 2; i++)
+        if (isp[i]) pr[npr++] = (uint32_t)i;
+    for (int t = 0; t < threads; t++) {
+        ws[t].isp = isp; ws[t].pr = pr; ws[t].npr = npr;
+        ws[t].lo_e = lo_e; ws[t].hi = hi; ws[t].tid = t; ws[t].nthreads = threads; ws[t].out = out;
+        pthread_create(&th[t], NULL, cn_main, &ws[t]);
+    }
+    for (int t = 0; t < threads; t++) pthread_join(th[t], NULL);
+    free(isp); free(pr); free(th); free(ws);
+    return 0;
 }
 
 int or_nbins(void) { return OR_NBINS; }

@@ -19,7 +19,7 @@ LIB = os.path.join(HERE, "liboracle.so")
 NBINS = 6544
 U64_MAX = (1 << 64) - 1
 FIELDS = ("evens", "verified", "fastpath_unresolved", "unresolved",
-          "first_unresolved_n", "max_pmin", "max_pmin_n", "sum_pmin", "chk", "chk192")
+          "first_unresolved_n", "max_pmin", "max_pmin_n", "sum_pmin", "chk")
 # the aggregates libgb's result vector carries (chk = sum n*p_min needs the per-n
 # values: tests compare it through dumps, see chk_of_dump)
 AGG_FIELDS = tuple(f for f in FIELDS if f != "chk")
@@ -30,8 +30,7 @@ class OrResult(ctypes.Structure):
                 ("fastpath_unresolved", ctypes.c_int64), ("unresolved", ctypes.c_int64),
                 ("first_unresolved_n", ctypes.c_int64), ("max_pmin", ctypes.c_int64),
                 ("max_pmin_n", ctypes.c_int64), ("sum_pmin", ctypes.c_int64),
-                ("chk", ctypes.c_uint64), ("chk192", ctypes.c_uint64),
-                ("hist", ctypes.c_int64 * NBINS)]
+                ("chk", ctypes.c_uint64), ("hist", ctypes.c_int64 * NBINS)]
 
 
 def build(force: bool = False) -> str:
@@ -64,6 +63,8 @@ def lib():
         L.or_sieve_window.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p]
         L.or_prime_pi.restype = ctypes.c_uint64
         L.or_prime_pi.argtypes = [ctypes.c_uint64, ctypes.c_int]
+        L.or_partition_counts.restype = ctypes.c_int
+        L.or_partition_counts.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p]
         L.or_result_size.restype = ctypes.c_size_t
         assert L.or_result_size() == ctypes.sizeof(OrResult)
         _lib = L
@@ -128,3 +129,14 @@ def verify(lo: int, hi: int, p_fast: int = 65521, cap: int = U64_MAX,
     if ch is not None:
         out["chunk_chk"] = ch
     return out, d
+
+
+def partition_counts(lo: int, hi: int, threads: int | None = None) -> np.ndarray:
+    """c(n) = #{p prime <= n/2 : n - p prime} for every even n in [lo_e, hi)
+    (NEXT-4; reading R13), as a uint64 array indexed (n - lo_e)/2."""
+    out = np.zeros(n_evens(lo, hi), dtype=np.uint64)
+    if out.size:
+        rc = lib().or_partition_counts(lo, hi, threads or default_threads(), out.ctypes.data)
+        if rc != 0:
+            raise RuntimeError(f"or_partition_counts rc={rc}")
+    return out

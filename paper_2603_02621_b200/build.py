@@ -11,7 +11,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libgb.so")
-SOURCES = ["gb_kernels.cu", "gb_verify.cu", "gb_pern.cu", "gb_api.cu"]
+SOURCES = ["gb_kernels.cu", "gb_verify.cu", "gb_pern.cu", "gb_counts.cu", "gb_api.cu"]
 HEADERS = ["gb_internal.h", "mr64.cuh", "gb_device.cuh"]
 
 NVCC_FLAGS = [

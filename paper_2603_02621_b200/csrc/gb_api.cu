@@ -400,10 +400,9 @@ gb_status gb_result_init(int64_t *d_result, void *stream)
 gb_status gb_result_finalize(int64_t *d_result, void *stream)
 {
     if (!d_result || ((uintptr_t)d_result & 7)) return GB_EINVAL;
+    (void)stream;
     int dev = -1;
-    if (!pointer_device(d_result, dev)) return GB_EINVAL;
-    DeviceGuard g(dev);
-    return launch_result_finalize(d_result, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
+    return pointer_device(d_result, dev) ? GB_OK : GB_EINVAL;
 }
 
 gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_max,
@@ -626,6 +625,20 @@ gb_status gb_verify_range_resident(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32
     a.result = d_result;
     a.dump = d_pmin_dump;
     return launch_pern(a, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
+}
+
+gb_status gb_partition_counts(gb_ctx *ctx, uint64_t lo, uint64_t hi, const uint64_t *d_bits, uint64_t n_words,
+                              uint64_t *d_counts, void *stream)
+{
+    if (!ctx || ((uintptr_t)d_bits & 7) || ((uintptr_t)d_counts & 7)) return GB_EINVAL;
+    if (lo > hi || hi > GB_COUNTS_HI_LIMIT) return GB_EINVAL;
+    const uint64_t lo_e = lo < 4 ? 4 : lo + (lo & 1);
+    if (hi <= lo_e) return GB_OK;                            // empty range: no launch
+    if (!d_bits || !d_counts) return GB_EINVAL;
+    if (n_words > (1ull << 58) || 3 + 128 * n_words < hi) return GB_EINVAL;   // every odd q < hi present
+    DeviceGuard g(ctx->device);
+    return launch_counts(d_bits, n_words, lo_e, hi, d_counts, ctx->num_sms, S(stream)) == cudaSuccess ? GB_OK
+                                                                                                      : GB_ECUDA;
 }
 
 gb_status gb_single_check(gb_ctx *ctx, uint64_t n, uint64_t p_limit, uint64_t *d_out, void *stream)

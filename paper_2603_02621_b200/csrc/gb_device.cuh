@@ -104,7 +104,7 @@ __device__ __forceinline__ uint32_t bin_of_prime(uint64_t p, const uint32_t *pri
 }
 
 struct Acc {
-    uint64_t evens = 0, verified = 0, fast_unres = 0, unres = 0, sum = 0, chk = 0;
+    uint64_t evens = 0, verified = 0, fast_unres = 0, unres = 0, sum = 0;
     uint64_t key = 0, first_unres = UINT64_MAX;
     uint64_t praw = 0;        // largest p_min above GB_KEY_PMAX (the key's p field saturates)
 };
@@ -126,7 +126,7 @@ __device__ __forceinline__ void flush_acc(const Acc &acc, int64_t *result, int l
         return v;
     };
     const uint64_t ev = wsum(acc.evens), vf = wsum(acc.verified), fu = wsum(acc.fast_unres);
-    const uint64_t un = wsum(acc.unres), sm = wsum(acc.sum), ck = wsum(acc.chk);
+    const uint64_t un = wsum(acc.unres), sm = wsum(acc.sum);
     const uint64_t ky = wmax(acc.key), fr = wmin(acc.first_unres), pr = wmax(acc.praw);
     unsigned long long *R = (unsigned long long *)result;
     if (lane == 0) {
@@ -135,7 +135,6 @@ __device__ __forceinline__ void flush_acc(const Acc &acc, int64_t *result, int l
         if (fu) atomicAdd(R + GB_R_FASTPATH_UNRESOLVED, fu);
         if (un) atomicAdd(R + GB_R_UNRESOLVED, un);
         if (sm) atomicAdd(R + GB_R_SUM_PMIN, sm);
-        if (ck) atomicAdd(R + GB_R_CHK_RAW, ck);
         if (ky) atomicMax(R + GB_R_MAX_KEY, ky);
         if (pr) atomicMax(R + GB_R_MAX_PMIN_RAW, pr);
         if (fr != UINT64_MAX) atomicMin(R + GB_R_FIRST_UNRESOLVED_N, fr);

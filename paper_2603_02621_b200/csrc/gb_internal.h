@@ -154,11 +154,12 @@ cudaError_t launch_scan(uint64_t *blk, uint64_t n_blk, cudaStream_t st);
 cudaError_t launch_scatter(const uint64_t *bits, uint64_t n_words, const uint64_t *blk,
                            uint32_t *primes, uint64_t *magic, uint4 *pk, cudaStream_t st);
 cudaError_t launch_result_init(int64_t *res, cudaStream_t st);
-cudaError_t launch_result_finalize(int64_t *res, cudaStream_t st);
 cudaError_t launch_verify(const VerifyArgs &a, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_large(const LargeArgs &a, int num_sms, cudaStream_t st);   // mask fill + marking
 cudaError_t launch_is_prime(const uint64_t *x, uint8_t *out, uint64_t n, const uint64_t *bits,
                             uint64_t R, cudaStream_t st);
+cudaError_t launch_counts(const uint64_t *bits64, uint64_t n_words64, uint64_t lo_e, uint64_t hi, uint64_t *counts,
+                          int num_sms, cudaStream_t st);
 cudaError_t configure_verify();
 cudaError_t ensure_dyn_smem(const void *kernel, int bytes, std::atomic<uint64_t> &done);
 cudaError_t launch_sieve_out(const SieveOutArgs &a, int grid, size_t smem, cudaStream_t st);

@@ -413,14 +413,6 @@ __global__ void result_init_kernel(int64_t *r)
     }
 }
 
-__global__ void result_finalize_kernel(int64_t *r)
-{
-    const uint64_t c = (uint64_t)r[GB_R_CHK_RAW];
-    r[GB_R_CHK_LO32] += (int64_t)(c & 0xffffffffu);
-    r[GB_R_CHK_HI32] += (int64_t)(c >> 32);
-    r[GB_R_CHK_RAW] = 0;
-}
-
 __global__ void is_prime_kernel(const uint64_t *x, uint8_t *out, uint64_t n)
 {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -495,13 +487,6 @@ cudaError_t launch_large(const LargeArgs &a, int num_sms, cudaStream_t st)
 cudaError_t launch_result_init(int64_t *res, cudaStream_t st)
 {
     result_init_kernel<<<1, 256, 0, st>>>(res);
-    count_launch();
-    return cudaGetLastError();
-}
-
-cudaError_t launch_result_finalize(int64_t *res, cudaStream_t st)
-{
-    result_finalize_kernel<<<1, 1, 0, st>>>(res);
     count_launch();
     return cudaGetLastError();
 }

@@ -96,7 +96,6 @@ __global__ void __launch_bounds__(256) pern_kernel(const __grid_constant__ PerNA
             if (pmin) {
                 acc.verified += 1;
                 acc.sum += pmin;
-                acc.chk += pmin * (n / 192);                      // DESIGN.md R6 weight
                 note_key(acc, pmin, n, a.origin);
                 hist_add(sh_hist, a.result, bin, 1);
             } else {

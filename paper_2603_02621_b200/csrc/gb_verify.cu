@@ -144,6 +144,15 @@ __device__ __forceinline__ void first_hits6(uint32_t p, uint32_t rA, uint32_t rB
     ob = (uint32_t)(base + (rB >= rem ? rB - rem : rB + p - rem));
 }
 
+// class-B offset of a steady prime from its class-A offset (both residues mod p):
+// m == rB and m == rA (mod p) differ by rB - rA
+__device__ __forceinline__ uint32_t class_b_off(uint32_t oa, uint4 k)
+{
+    const uint32_t d = k.w >= k.z ? k.w - k.z : k.w + k.x - k.z;
+    const uint32_t ob = oa + d;
+    return ob >= k.x ? ob - k.x : ob;
+}
+
 // next tile's first hit (the window moves up by tile_m)
 __device__ __forceinline__ uint32_t next_off6(uint32_t off, uint32_t p, uint32_t tm, uint32_t tile_m)
 {
@@ -346,8 +355,10 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
     const uint32_t b1 = i_b1 < b2 ? b2 : (i_b1 < s_end ? i_b1 : s_end);
     const uint64_t cpol = carry_policy();
     uint32_t *__restrict__ cA = cy->off;                 // this CTA's carry row, class A
-    uint32_t *__restrict__ cB = cy->off + cy->stride;    // class B
     const uint4 *__restrict__ pkp = sp.pk;
+    // Steady primes carry only their class-A offset: both progressions step by the
+    // same p per tile, so ob = oa + (rB - rA) mod p (both offsets are residues in
+    // [0, p) once p^2 lies below the window) -- half the carry-row traffic.
     constexpr int kB = 2;             // steady primes in flight per thread (1 or 4: slower)
     // steady primes with p <= full window / 2: hit loops (>= 2 hits per class)
     for (uint32_t w0 = b_begin + (tid & ~31u); w0 < b2; w0 += kB * nt) {   // warp-uniform trips
@@ -361,7 +372,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
                 const uint4 q = __ldg(pkp + pi);
                 pt[k] = make_uint2(q.x, tile_mod<DEF_TILE>(cy, q));
                 oa[k] = carry_ld(cA + pi, cpol);
-                ob[k] = carry_ld(cB + pi, cpol);
+                ob[k] = class_b_off(oa[k], q);
             } else {
                 pt[k] = make_uint2(1, 0);
                 oa[k] = ob[k] = nbits;
@@ -386,10 +397,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
                 for (; bb < nbits; bb += p) clear_bit(sB, bb);
             }
             const uint32_t pi = p0 + k * nt;
-            if (pi < b2) {
-                carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
-                carry_st(cB + pi, ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm, cpol);
-            }
+            if (pi < b2) carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
         }
         __syncwarp();   // reconverge: the per-lane hit loops diverge
     }
@@ -406,7 +414,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
                 pp[k] = q.x;
                 tt[k] = tile_mod<DEF_TILE>(cy, q);
                 oa[k] = carry_ld(cA + pi, cpol);
-                ob[k] = carry_ld(cB + pi, cpol);
+                ob[k] = class_b_off(oa[k], q);
             } else {
                 pp[k] = nbits; tt[k] = 0;
                 oa[k] = ob[k] = nbits;
@@ -420,10 +428,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             if (ob[k] < nbits) clear_bit(sB, ob[k]);
             if (ob[k] + p < nbits) clear_bit(sB, ob[k] + p);
             const uint32_t pi = p0 + k * nt;
-            if (pi < b1) {
-                carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
-                carry_st(cB + pi, ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm, cpol);
-            }
+            if (pi < b1) carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
         }
     }
     // steady primes with p > a full window: at most 1 hit per class
@@ -438,7 +443,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
                 pp[k] = q.x;
                 tt[k] = tile_mod<DEF_TILE>(cy, q);
                 oa[k] = carry_ld(cA + pi, cpol);
-                ob[k] = carry_ld(cB + pi, cpol);
+                ob[k] = class_b_off(oa[k], q);
             } else {
                 pp[k] = nbits; tt[k] = 0;
                 oa[k] = ob[k] = nbits;
@@ -450,10 +455,7 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             if (oa[k] < nbits) clear_bit(sA, oa[k]);
             if (ob[k] < nbits) clear_bit(sB, ob[k]);
             const uint32_t pi = p0 + k * nt;
-            if (pi < s_end) {
-                carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
-                carry_st(cB + pi, ob[k] >= tm ? ob[k] - tm : ob[k] + p - tm, cpol);
-            }
+            if (pi < s_end) carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
         }
     }
     for (uint32_t pi = s_end + tid; pi < sp.n_use; pi += nt) {
@@ -485,7 +487,6 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
 struct Lane6 {
     const uint32_t *wa, *wb;   // class A / B window word aligned with this U word
     uint32_t U;                // unresolved evens of the word
-    uint32_t word_sum;         // sum of p_min of bits resolved in the unrolled range
     uint32_t lb;               // 1 + index of the last 8-candidate block with a hit (0 = none)
     uint32_t lu;               // U at the start of that block
     uint32_t *dump_w;          // dump entry of bit 0 (bit b at dump_w[3b]) -- DUMP only
@@ -503,7 +504,6 @@ __device__ __forceinline__ uint32_t mark_step(Lane6 &m)
     const uint32_t nw = m.U & S;              // n resolved now: n - P prime, no smaller p worked
     m.U ^= nw;
     const uint32_t c = __popc(nw);
-    m.word_sum += c * P;
     if constexpr (DUMP) {
         uint32_t x = nw;
         while (x) {
@@ -581,7 +581,6 @@ static_assert(31 + 32 * kW <= kQueue, "survivor queue capacity");
 struct LaneQ {
     const uint32_t *wa, *wb;   // class A / B window words aligned with word 0 (word k at +32k)
     uint32_t U[kW];
-    uint32_t ws[kW];           // sum of p_min of resolved bits, per word
     uint32_t lb[kW], lu[kW];   // TRACK: last block with a hit and U at its start
     uint32_t *dump0;           // DUMP: dump entry of bit 0 of word 0 (word k at +3072k, bit b at +3b)
 };
@@ -598,7 +597,6 @@ __device__ __forceinline__ uint32_t qstep(LaneQ &m, int k)
     const uint32_t nw = m.U[k] & S;
     m.U[k] ^= nw;
     const uint32_t c = __popc(nw);
-    m.ws[k] += c * P;
     if constexpr (DUMP) {
         uint32_t x = nw;
         while (x) {
@@ -663,7 +661,6 @@ template <int S>
 struct LaneR {
     const uint32_t *wa[S], *wb[S];  // class A / B window word aligned with U word k
     uint32_t U[S];
-    uint32_t ws[S];
     uint32_t lb[S], lu[S];
     uint32_t li[S];                 // word index within the tile
     uint32_t *dump[S];              // DUMP: dump entry of bit 0 of word k (bit b at +3b)
@@ -681,7 +678,6 @@ __device__ __forceinline__ uint32_t rstep(LaneR<S> &m, int k)
     const uint32_t nw = m.U[k] & S_;
     m.U[k] ^= nw;
     const uint32_t c = __popc(nw);
-    m.ws[k] += c * P;
     if constexpr (DUMP) {
         uint32_t x = nw;
         while (x) {
@@ -842,7 +838,7 @@ __device__ __forceinline__ void replay_key_r(const LaneR<S> &m, uint64_t u0, con
 // candidates past the unrolled tables (runtime loop over the resident list, class
 // filtered), then the exhaustive on-GPU fallback; folds the word into acc
 template <int A, bool DUMP>
-__device__ __forceinline__ void finish_word(uint32_t U, uint64_t word_sum, uint32_t j0, const uint32_t *wa,
+__device__ __forceinline__ void finish_word(uint32_t U, uint32_t j0, const uint32_t *wa,
                                             const uint32_t *wb, uint64_t u, uint32_t *sh_hist,
                                             const VerifyArgs &a, Acc &acc, int lane)
 {
@@ -859,7 +855,7 @@ __device__ __forceinline__ void finish_word(uint32_t U, uint64_t word_sum, uint3
         const uint32_t c = __popc(nw);
         if (nw) {
             U ^= nw;
-            word_sum += (uint64_t)c * p;
+            acc.sum += (uint64_t)c * p;
             lastp = p; lastb = nw;
             if (DUMP) {
                 uint32_t x = nw;
@@ -890,7 +886,7 @@ __device__ __forceinline__ void finish_word(uint32_t U, uint64_t word_sum, uint3
         if (lane == L) {
             U &= ~(1u << bit);
             if (p) {
-                word_sum += p;
+                acc.sum += p;
                 hist_add(sh_hist, a.result, bin_of_prime(p, a.sp.primes, a.n_base), 1);
                 note_key(acc, p, n, a.origin);
             } else {
@@ -901,8 +897,6 @@ __device__ __forceinline__ void finish_word(uint32_t U, uint64_t word_sum, uint3
             if (DUMP) a.dump[(n - a.lo_e) / 2] = (uint32_t)p;
         }
     }
-    acc.sum += word_sum;
-    acc.chk += word_sum * u;                 // CHK weight floor(n / 192) = u for every bit
 }
 
 template <int A>
@@ -1014,13 +1008,12 @@ struct ClassWork {
         m.wa = wA + halo + li;
         m.wb = wB + halo + li;
         m.U = U;
-        m.word_sum = 0;
         m.lb = 0; m.lu = 0;
         m.dump_w = DUMP ? a.dump + ((int64_t)(192 * u + A) - (int64_t)a.lo_e) / 2 : nullptr;
         phase2<A, kP1, DUMP>(m, sh.histc[A / 2], lane);
         replay_key<A>(m, u, a, best_p, acc);
         constexpr uint32_t j_next = kTab[A / 2].bin[kK - 1] - 1;   // odd-list index after the table
-        finish_word<A, DUMP>(m.U, m.word_sum, j_next, m.wa, m.wb, u, sh.hist, a, acc, lane);
+        finish_word<A, DUMP>(m.U, j_next, m.wa, m.wb, u, sh.hist, a, acc, lane);
     }
 
     // one phase-1 round: words pair*32kW + 32k + lane (k < kW) of class A
@@ -1044,7 +1037,6 @@ struct ClassWork {
 #pragma unroll
             for (int k = 0; k < kW; ++k) {
                 m.U[k] = FULL;
-                m.ws[k] = 0;
                 if (TRACK) { m.lb[k] = 0; m.lu[k] = 0; }
             }
             acc.evens += 32 * kW;
@@ -1056,16 +1048,10 @@ struct ClassWork {
                 acc.evens += __popc(U);
                 if (k == 0) U = take_special<A, DUMP>(U, u0 + li, sh.hist, a, acc);
                 m.U[k] = U;
-                m.ws[k] = 0;
                 if (TRACK) { m.lb[k] = 0; m.lu[k] = 0; }
             }
         }
         phase1q<A, 0, kC1, DUMP, TRACK>(m, sh.histc[A / 2], lane);
-#pragma unroll
-        for (int k = 0; k < kW; ++k) {
-            acc.sum += m.ws[k];
-            acc.chk += (uint64_t)m.ws[k] * (u0 + li0 + 32 * k);
-        }
         if (TRACK) replay_key_q<A>(m, u0 + li0, a, best_p, acc);
         // survivors of candidates [0, kC1): staged past the queue's live entries,
         // then compacted to 2 (or 1) words per lane for candidates [kC1, kP1)
@@ -1108,17 +1094,11 @@ struct ClassWork {
             m.U[k] = U;
             m.wa[k] = wA + halo + li;
             m.wb[k] = wB + halo + li;
-            m.ws[k] = 0;
             if (TRACK) { m.lb[k] = 0; m.lu[k] = 0; }
             if (DUMP) m.dump[k] = a.dump + ((int64_t)(192 * (u0 + li) + A) - (int64_t)a.lo_e) / 2;
         }
         __syncwarp();                          // staged entries read before any append
         phase1r<A, kC1, S, DUMP, TRACK>(m, sh.histc[A / 2], lane);
-#pragma unroll
-        for (int k = 0; k < S; ++k) {
-            acc.sum += m.ws[k];
-            acc.chk += (uint64_t)m.ws[k] * (u0 + m.li[k]);
-        }
         if (TRACK) replay_key_r<A, S>(m, u0, a, best_p, acc);
 #pragma unroll
         for (int k = 0; k < S; ++k) {
@@ -1154,7 +1134,7 @@ struct ClassWork {
                 uint32_t U = li < tw ? valid_mask<A>(u, a) : 0u;
                 acc.evens += __popc(U);
                 if (k == 0) U = take_special<A, DUMP>(U, u, sh.hist, a, acc);
-                finish_word<A, DUMP>(U, 0, 0, wA + halo + li, wB + halo + li, u, sh.hist, a, acc, lane);
+                finish_word<A, DUMP>(U, 0, wA + halo + li, wB + halo + li, u, sh.hist, a, acc, lane);
             }
         }
     }
@@ -1200,8 +1180,10 @@ __device__ __forceinline__ void mark_tile(Shared6 &sh, uint32_t &next_round, uin
     flush_queue<DUMP, UNROLL>(qcls, sh, qn, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
 }
 
-// shared histograms -> result vector (all threads; callers barrier around it)
-__device__ __forceinline__ void flush_hist(Shared6 &sh, const VerifyArgs &a, int tid)
+// shared histograms -> result vector (all threads; callers barrier around it).  The
+// unrolled candidates' counts also give their share of sum p_min (count x p): the
+// marking loops keep no per-word sums (every other path adds to acc.sum directly).
+__device__ __forceinline__ void flush_hist(Shared6 &sh, const VerifyArgs &a, Acc &acc, int tid)
 {
     unsigned long long *R = (unsigned long long *)a.result;
     for (int i = tid; i < kHistSmem; i += kThreads) {
@@ -1214,6 +1196,7 @@ __device__ __forceinline__ void flush_hist(Shared6 &sh, const VerifyArgs &a, int
     for (int i = tid; i < 3 * kK; i += kThreads) {
         const uint32_t v = (&sh.histc[0][0])[i];
         if (v) {
+            acc.sum += (uint64_t)v * c_tab[i / kK].p[i % kK];
             atomicAdd(R + GB_R_HIST + c_tab[i / kK].bin[i % kK], (unsigned long long)v);
             (&sh.histc[0][0])[i] = 0;
         }
@@ -1275,7 +1258,7 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant_
         mark_tile<DUMP, UNROLL>(sh, sh.next_round[0], u0, tw, wA, wB, halo, a, acc, best_p, lane, warp);
         // per-tile flush of the shared histograms keeps their 32-bit bins exact
         __syncthreads();
-        flush_hist(sh, a, tid);
+        flush_hist(sh, a, acc, tid);
     }
     acc.verified = acc.evens - acc.unres;
 

@@ -42,7 +42,7 @@ def reduce_result(result: torch.Tensor, group=None) -> None:
     """In-place cross-rank reduction of a FINALIZED result vector (int64)."""
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return
-    s1 = result[gb.R_EVENS:gb.R_CHK_HI32 + 1]            # SUM fields 1..7
+    s1 = result[gb.R_EVENS:gb.R_SUM_PMIN + 1]            # SUM fields 1..5
     s2 = result[gb.R_HIST:gb.R_HIST + gb.NBINS]          # SUM hist
     mx = torch.stack([result[gb.R_MAX_KEY], result[gb.R_MAX_PMIN_RAW]])
     mn = result[gb.R_FIRST_UNRESOLVED_N:gb.R_FIRST_UNRESOLVED_N + 1]
@@ -50,7 +50,7 @@ def reduce_result(result: torch.Tensor, group=None) -> None:
     dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
     dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
     dist.all_reduce(mn, op=dist.ReduceOp.MIN, group=group)
-    result[gb.R_EVENS:gb.R_CHK_HI32 + 1] = sums[:s1.numel()]
+    result[gb.R_EVENS:gb.R_SUM_PMIN + 1] = sums[:s1.numel()]
     result[gb.R_HIST:gb.R_HIST + gb.NBINS] = sums[s1.numel():]
     result[gb.R_MAX_KEY] = mx[0]
     result[gb.R_MAX_PMIN_RAW] = mx[1]

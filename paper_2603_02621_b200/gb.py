@@ -32,11 +32,8 @@ R_VERIFIED = _c_int(_defs["GB_R_VERIFIED"])
 R_FASTPATH_UNRESOLVED = _c_int(_defs["GB_R_FASTPATH_UNRESOLVED"])
 R_UNRESOLVED = _c_int(_defs["GB_R_UNRESOLVED"])
 R_SUM_PMIN = _c_int(_defs["GB_R_SUM_PMIN"])
-R_CHK_LO32 = _c_int(_defs["GB_R_CHK_LO32"])
-R_CHK_HI32 = _c_int(_defs["GB_R_CHK_HI32"])
 R_FIRST_UNRESOLVED_N = _c_int(_defs["GB_R_FIRST_UNRESOLVED_N"])
 R_MAX_KEY = _c_int(_defs["GB_R_MAX_KEY"])
-R_CHK_RAW = _c_int(_defs["GB_R_CHK_RAW"])
 R_MAX_PMIN_RAW = _c_int(_defs["GB_R_MAX_PMIN_RAW"])
 R_HIST = _c_int(_defs["GB_R_HIST"])
 NBINS = _c_int(_defs["GB_NBINS"])
@@ -68,12 +65,13 @@ _sigs = {
     "gb_verify_range_pern": (ctypes.c_int, [_vp, _u64, _u64, _u32, _vp, _vp, _vp]),
     "gb_verify_range_resident": (ctypes.c_int, [_vp, _u64, _u64, _u32, _vp, _u64, _vp, _vp, _vp]),
     "gb_single_check": (ctypes.c_int, [_vp, _u64, _u64, _vp, _vp]),
+    "gb_partition_counts": (ctypes.c_int, [_vp, _u64, _u64, _vp, _u64, _vp, _vp]),
     "gb_is_prime_u64": (ctypes.c_int, [_vp, _vp, _u64, _vp]),
     "gb_launch_count": (_u64, []),
     "gb_status_string": (ctypes.c_char_p, [ctypes.c_int]),
 }
 for _name, (_res, _args) in _sigs.items():
-    _f = getattr(_lib, _name)
+    _f = getattr(_lib, _name)          # raises if the library lacks a declared entry point
     _f.restype = _res
     _f.argtypes = _args
 
@@ -157,6 +155,11 @@ def gb_single_check(ctx: int, n: int, p_limit: int, d_out, stream) -> None:
     _check(_lib.gb_single_check(ctx, n, p_limit, _ptr(d_out), _ptr_stream(stream)), "gb_single_check")
 
 
+def gb_partition_counts(ctx: int, lo: int, hi: int, d_bits, n_words: int, d_counts, stream) -> None:
+    _check(_lib.gb_partition_counts(ctx, lo, hi, _ptr(d_bits), n_words, _ptr(d_counts), _ptr_stream(stream)),
+           "gb_partition_counts")
+
+
 def gb_verify_range_ex(ctx: int, lo: int, hi: int, p_max: int, cap: int, d_result, d_dump,
                        stream) -> None:
     _check(_lib.gb_verify_range_ex(ctx, lo, hi, p_max, cap, _ptr(d_result), _ptr(d_dump),
@@ -196,14 +199,13 @@ def _ptr_stream(stream) -> int | None:
 # ---- result decoding (host side, plain integer bookkeeping) ------------------
 def decode_result(words, origin: int = 0) -> dict:
     """Decode a finalized GB_RESULT_WORDS int64 vector into named fields.
-    chk192 = sum p_min(n) * floor(n/192) mod 2^64 (the block checksum the kernels
-    accumulate; the exact sum n * p_min comes from a per-n dump).  If some p_min
+    (The exact sum n * p_min, the position-sensitive check, comes from a per-n
+    dump; the result vector carries no checksum.)  If some p_min
     reached GB_KEY_PMAX the key's p field saturates: max_pmin is then the raw
     maximum and max_pmin_n is -1 (unknown)."""
     w = [int(x) for x in (words.tolist() if hasattr(words, "tolist") else words)]
     if w[R_VERSION] != RESULT_VERSION:
         raise ValueError("result vector has a bad version word (not initialised?)")
-    chk = ((w[R_CHK_HI32] << 32) + w[R_CHK_LO32] + (w[R_CHK_RAW] & U64_MAX)) & U64_MAX
     key = w[R_MAX_KEY]
     if key:
         p = key >> KEY_SHIFT
@@ -217,7 +219,7 @@ def decode_result(words, origin: int = 0) -> dict:
         "evens": w[R_EVENS], "verified": w[R_VERIFIED],
         "fastpath_unresolved": w[R_FASTPATH_UNRESOLVED], "unresolved": w[R_UNRESOLVED],
         "first_unresolved_n": w[R_FIRST_UNRESOLVED_N], "max_pmin": max_p, "max_pmin_n": max_n,
-        "sum_pmin": w[R_SUM_PMIN], "chk192": chk,
+        "sum_pmin": w[R_SUM_PMIN],
     }
     out["hist"] = w[R_HIST:R_HIST + NBINS]
     return out

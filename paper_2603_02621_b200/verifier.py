@@ -89,6 +89,17 @@ class Verifier:
         self.stream.synchronize()
         return int(out.cpu()[0]) & ((1 << 64) - 1)
 
+    def partition_counts(self, lo: int, hi: int, bits: torch.Tensor | None = None) -> torch.Tensor:
+        """NEXT-4: c(n) for every even n in [lo_e, hi) (int64 tensor indexed (n - lo_e)/2).
+        bits: the odd bitset words [0, n) covering every odd q < hi (sieved here,
+        gb_sieve_segment, when not given; needs hi_max >= hi)."""
+        if bits is None:
+            bits = self.sieve_segment(0, (hi - 3 + 127) // 128)
+        e = 4 if lo < 4 else lo + (lo & 1)
+        out = torch.empty(max(0, (hi - e + 1) // 2), dtype=torch.int64, device=self.device)
+        gb.gb_partition_counts(self.ctx, lo, hi, bits, bits.numel(), out if out.numel() else None, self.stream)
+        return out
+
     def sieve_segment(self, word_lo: int, n_words: int) -> torch.Tensor:
         out = torch.empty(n_words, dtype=torch.int64, device=self.device)
         gb.gb_sieve_segment(self.ctx, word_lo, n_words, out, self.stream)

@@ -32,7 +32,7 @@ v.finalize(r)
 w = v.sieve_segment((lo - 3) // 128, (1 << a.span) // 128 - 2)
 torch.cuda.synchronize()
 d = v.decode(r)
-print({k: d[k] for k in ("evens", "verified", "fastpath_unresolved", "max_pmin", "max_pmin_n", "chk192")})
+print({k: d[k] for k in ("evens", "verified", "fastpath_unresolved", "max_pmin", "max_pmin_n", "sum_pmin")})
 if a.time:
     r2 = v.new_result()
     for _ in range(2):

@@ -77,8 +77,6 @@ def to_words(r, gb):
     w[gb.R_FASTPATH_UNRESOLVED] = r["fastpath_unresolved"]
     w[gb.R_UNRESOLVED] = r["unresolved"]
     w[gb.R_SUM_PMIN] = r["sum_pmin"]
-    w[gb.R_CHK_LO32] = r["chk192"] & 0xFFFFFFFF
-    w[gb.R_CHK_HI32] = r["chk192"] >> 32
     w[gb.R_FIRST_UNRESOLVED_N] = r["first_unresolved_n"]
     if r["max_pmin"]:
         w[gb.R_MAX_KEY] = (r["max_pmin"] << gb.KEY_SHIFT) | ((1 << gb.KEY_SHIFT) - 1 - r["max_pmin_n"] // 2)
@@ -115,7 +113,7 @@ def _worker(rank, world, port, lo, hi, q):
         if acc is None:
             acc = w
         else:   # per-rank accumulation rule (what repeated gb_verify_range calls do)
-            acc[1:8] += w[1:8]
+            acc[1:6] += w[1:6]
             acc[gb.R_HIST:] += w[gb.R_HIST:]
             acc[gb.R_MAX_KEY] = max(acc[gb.R_MAX_KEY], w[gb.R_MAX_KEY])
             acc[gb.R_FIRST_UNRESOLVED_N] = min(acc[gb.R_FIRST_UNRESOLVED_N], w[gb.R_FIRST_UNRESOLVED_N])

@@ -233,8 +233,6 @@ def test_golden_aggregates(V, N, name):
     doc = json.load(open(path))
     g = doc["result"]
     got, _ = V.run(4, int(float(N)) + 1, dump=False)
-    if "chk192" not in g:
-        pytest.skip("golden predates chk192")
     for k in oracle.AGG_FIELDS:
         assert got[k] == g[k], k
     hist = np.zeros(oracle.NBINS, np.int64)

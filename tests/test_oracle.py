@@ -117,7 +117,6 @@ def test_brute_force_small():
     assert r["sum_pmin"] == int(want.sum())
     ns = np.arange(4, hi, 2, dtype=np.uint64)
     assert r["chk"] == int((want.astype(np.uint64) * ns).sum()) & U64
-    assert r["chk192"] == int((want.astype(np.uint64) * (ns // 192)).sum()) & U64
     idx = prime_index_bins()
     h = np.zeros(oracle.NBINS, dtype=np.int64)
     for p in want:
@@ -212,11 +211,10 @@ def test_additivity_and_edges():
         for k in ("evens", "verified", "fastpath_unresolved", "unresolved", "sum_pmin"):
             acc[k] += r[k]
         acc["chk"] = (acc["chk"] + r["chk"]) & U64
-        acc["chk192"] = (acc["chk192"] + r["chk192"]) & U64
         acc["hist"] = acc["hist"] + r["hist"]
         if (r["max_pmin"], -r["max_pmin_n"]) > (acc["max_pmin"], -acc["max_pmin_n"]):
             acc["max_pmin"], acc["max_pmin_n"] = r["max_pmin"], r["max_pmin_n"]
-    for k in ("evens", "verified", "sum_pmin", "chk", "chk192", "max_pmin", "max_pmin_n"):
+    for k in ("evens", "verified", "sum_pmin", "chk", "max_pmin", "max_pmin_n"):
         assert acc[k] == full[k], k
     assert np.array_equal(acc["hist"], full["hist"])
     # empty / degenerate ranges
@@ -297,3 +295,51 @@ def test_golden_c5_window_consistency():
     assert sum(g["hist"].values()) == g["evens"]
     assert 3191 <= g["max_pmin"] <= 9781
     assert 4 * 10**18 - 10**11 <= g["max_pmin_n"] < 4 * 10**18
+
+
+# ---------------------------------------------------------------- c(n) (NEXT-4)
+def test_partition_counts_hand_values():
+    """c(n) = #{p prime <= n/2 : n - p prime} (R13): 4 = 2+2; 10 = 3+7 = 5+5;
+    100 = 3+97 = 11+89 = 17+83 = 29+71 = 41+59 = 47+53."""
+    c = oracle.partition_counts(4, 101)
+    want = {4: 1, 6: 1, 8: 1, 10: 2, 12: 1, 14: 2, 16: 2, 18: 2, 20: 2, 22: 3, 100: 6}
+    for n, v in want.items():
+        assert int(c[(n - 4) // 2]) == v, n
+
+
+def test_partition_counts_vs_convolution():
+    """r(n) = number of ORDERED prime pairs (p, q), p + q = n, is the self-convolution of
+    the prime indicator (numpy's convolve: a library routine, not the oracle's loop);
+    c(n) = (r(n) + [n/2 prime]) / 2."""
+    N = 40000
+    P = np.zeros(N + 1, dtype=np.int64)
+    for x in range(2, N + 1):
+        P[x] = td_prime(x)
+    r = np.convolve(P, P)[: N + 1]
+    c = oracle.partition_counts(4, N + 1)
+    n = np.arange(4, N + 1, 2)
+    want = (r[n] + P[n // 2]) // 2
+    assert np.array_equal(c.astype(np.int64), want)
+
+
+def test_partition_counts_sum_identity():
+    """sum of c(n) over even n <= N counts the unordered prime pairs p <= q with
+    p + q <= N and p + q even: 1 (2 + 2) + sum over odd primes p <= N/2 of
+    #{odd primes q : p <= q <= N - p} -- prefix counts of a test-local sieve; also
+    an odd lo and a window at 1e7."""
+    N = 10**6
+    s = np.ones(N + 1, dtype=bool)
+    s[:2] = False
+    for i in range(2, 1001):
+        if s[i]:
+            s[i * i::i] = False
+    odd = s.copy()
+    odd[2] = False
+    pref = np.cumsum(odd)
+    ps = np.flatnonzero(odd[: N // 2 + 1])
+    want = 1 + int((pref[N - ps] - pref[ps - 1]).sum())
+    c = oracle.partition_counts(4, N + 1)
+    assert int(c.sum()) == want
+    assert int(c[-1]) == 5402                       # c(10^6), the window end
+    w = oracle.partition_counts(10**6 - 999, 10**6 + 1)
+    assert np.array_equal(w, c[-500:])
