@@ -28,7 +28,7 @@ from oracle import oracle  # noqa: E402
 
 U64 = (1 << 64) - 1
 CHUNK_EVENS = 1 << 24
-CHK_DEF = "chk = sum n*p_min(n) mod 2^64 (SURVEY.md 8(b)); chk192 = sum p_min(n)*floor(n/192) mod 2^64"
+CHK_DEF = "chk = sum n*p_min(n) mod 2^64 (SURVEY.md 8(b))"
 
 
 def merge(a, b):
@@ -38,7 +38,6 @@ def merge(a, b):
     for k in ("evens", "verified", "fastpath_unresolved", "unresolved", "sum_pmin"):
         out[k] = a[k] + b[k]
     out["chk"] = (a["chk"] + b["chk"]) & U64
-    out["chk192"] = (a["chk192"] + b["chk192"]) & U64
     out["first_unresolved_n"] = min(a["first_unresolved_n"], b["first_unresolved_n"])
     if (b["max_pmin"], -b["max_pmin_n"]) > (a["max_pmin"], -a["max_pmin_n"]):
         out["max_pmin"], out["max_pmin_n"] = b["max_pmin"], b["max_pmin_n"]
