@@ -482,6 +482,27 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
 }
 
 // ---------------------------------------------------------------------------
+// accumulators of the verify kernel: every count in per-CTA shared memory (shared
+// atomics: once per round for the evens, per tile for the histogram share of
+// sum p_min, else only on the cold paths), the max key per thread in registers --
+// the hot marking loops hold no accumulator registers
+// ---------------------------------------------------------------------------
+struct CtaAcc {
+    unsigned long long evens, fast_unres, unres, sum, praw, first_unres;
+};
+struct VAcc {
+    uint64_t key = 0;          // largest make_key(p_min, n) this thread saw
+    CtaAcc *c;
+};
+
+__device__ __forceinline__ void vnote_key(VAcc &acc, uint64_t p, uint64_t n, uint64_t origin)
+{
+    const uint64_t key = make_key(p, n, origin);
+    if (key > acc.key) acc.key = key;
+    if (p >= GB_KEY_PMAX) atomicMax(&acc.c->praw, (unsigned long long)p);
+}
+
+// ---------------------------------------------------------------------------
 // the inverted marking loop on one U word per lane
 // ---------------------------------------------------------------------------
 struct Lane6 {
@@ -501,22 +522,23 @@ __device__ __forceinline__ uint32_t mark_step(Lane6 &m)
     constexpr uint32_t WB = T.shift & 31;
     const uint32_t *src = T.src ? m.wb : m.wa;
     const uint32_t S = __funnelshift_l(src[-(WA + 1)], src[-WA], WB);
-    const uint32_t nw = m.U & S;              // n resolved now: n - P prime, no smaller p worked
-    m.U ^= nw;
-    const uint32_t c = __popc(nw);
     if constexpr (DUMP) {
-        uint32_t x = nw;
+        uint32_t x = m.U & S;                 // n resolved now: n - P prime, no smaller p worked
         while (x) {
             const int b = __ffs(x) - 1;
             x &= x - 1;
             m.dump_w[3 * b] = P;
         }
     }
-    return c;
+    m.U &= ~S;
+    return __popc(m.U);                       // A_J: still unresolved after P (see hist8)
 }
 
-// per-warp counts of 8 candidates -> class histogram (two counts per REDUX:
-// 16-bit fields, per warp and candidate <= 2048 hits)
+// Per-warp counts of 8 candidates -> class histogram (two counts per REDUX: 16-bit
+// fields, per warp and candidate <= 32 kW 32 = 3072).  The counts are A_J = evens
+// still unresolved AFTER candidate J (one AND-NOT + POPC per word and candidate,
+// no separate "resolved now" word); h[J] accumulates A_J and h[-1] the evens that
+// enter the table, so flush_hist takes hist[J] = A_{J-1} - A_J.
 __device__ __forceinline__ void hist8(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t c4,
                                       uint32_t c5, uint32_t c6, uint32_t c7, uint32_t *h, int lane)
 {
@@ -545,34 +567,6 @@ __device__ __forceinline__ void block8(Lane6 &m, uint32_t *h, int lane)
     hist8(c0, c1, c2, c3, c4, c5, c6, c7, h + J, lane);
 }
 
-template <int A, int J, bool DUMP>
-__device__ __forceinline__ void block8x2(Lane6 &m0, Lane6 &m1, uint32_t *h, int lane)
-{
-    const uint32_t U0 = m0.U, U1 = m1.U;
-    uint32_t c[8];
-    c[0] = mark_step<A, J + 0, DUMP>(m0); c[0] += mark_step<A, J + 0, DUMP>(m1);
-    c[1] = mark_step<A, J + 1, DUMP>(m0); c[1] += mark_step<A, J + 1, DUMP>(m1);
-    c[2] = mark_step<A, J + 2, DUMP>(m0); c[2] += mark_step<A, J + 2, DUMP>(m1);
-    c[3] = mark_step<A, J + 3, DUMP>(m0); c[3] += mark_step<A, J + 3, DUMP>(m1);
-    c[4] = mark_step<A, J + 4, DUMP>(m0); c[4] += mark_step<A, J + 4, DUMP>(m1);
-    c[5] = mark_step<A, J + 5, DUMP>(m0); c[5] += mark_step<A, J + 5, DUMP>(m1);
-    c[6] = mark_step<A, J + 6, DUMP>(m0); c[6] += mark_step<A, J + 6, DUMP>(m1);
-    c[7] = mark_step<A, J + 7, DUMP>(m0); c[7] += mark_step<A, J + 7, DUMP>(m1);
-    if (m0.U != U0) { m0.lb = J / 8 + 1; m0.lu = U0; }
-    if (m1.U != U1) { m1.lb = J / 8 + 1; m1.lu = U1; }
-    hist8(c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7], h + J, lane);
-}
-
-// phase 1: candidates [J, kP1) for two words per lane, no exit tests
-template <int A, int J, bool DUMP>
-__device__ __forceinline__ void phase1(Lane6 &m0, Lane6 &m1, uint32_t *h, int lane)
-{
-    if constexpr (J < kP1) {
-        block8x2<A, J, DUMP>(m0, m1, h, lane);
-        phase1<A, J + 8, DUMP>(m0, m1, h, lane);
-    }
-}
-
 // ---- phase 1 with kW words per lane (words li, li + 32, ..., li + 32(kW-1)) ----
 constexpr int kW = 3;            // phase-1 words per lane (2: slower)
 static_assert(kW * 32 * 32 < 65536, "16-bit packed per-warp counts");
@@ -586,7 +580,7 @@ struct LaneQ {
 };
 
 template <int A, int J, bool DUMP>
-__device__ __forceinline__ uint32_t qstep(LaneQ &m, int k)
+__device__ __forceinline__ void qstep(LaneQ &m, int k)
 {
     constexpr uint32_t P = kTab[A / 2].p[J];
     constexpr Trans T = trans(A, P);
@@ -594,27 +588,31 @@ __device__ __forceinline__ uint32_t qstep(LaneQ &m, int k)
     constexpr uint32_t WB = T.shift & 31;
     const uint32_t *src = (T.src ? m.wb : m.wa) + 32 * k;
     const uint32_t S = __funnelshift_l(src[-(WA + 1)], src[-WA], WB);
-    const uint32_t nw = m.U[k] & S;
-    m.U[k] ^= nw;
-    const uint32_t c = __popc(nw);
     if constexpr (DUMP) {
-        uint32_t x = nw;
+        uint32_t x = m.U[k] & S;
         while (x) {
             const int b = __ffs(x) - 1;
             x &= x - 1;
             m.dump0[3072 * k + 3 * b] = P;
         }
     }
-    return c;
+    m.U[k] &= ~S;
 }
 
+// A_J of the lane's kW = 3 words with 2 POPC instead of 3: a carry-save full adder
+// (sum = a ^ b ^ c, carry = maj(a, b, c): two LOP3) gives popc(a) + popc(b) + popc(c)
+// = popc(sum) + 2 popc(carry).  POPC issues at 16 lanes/clk/SM (a quarter of LOP3,
+// profiles/peaks_int.json) through the MIO queue the window loads also use: it,
+// not the ALU, bounds the marking loops (mio throttle, profiles/r02b_*).
 template <int A, int J, bool DUMP>
 __device__ __forceinline__ uint32_t qprime(LaneQ &m)
 {
-    uint32_t c = 0;
+    static_assert(kW == 3, "carry-save count of three words");
 #pragma unroll
-    for (int k = 0; k < kW; ++k) c += qstep<A, J, DUMP>(m, k);
-    return c;
+    for (int k = 0; k < kW; ++k) qstep<A, J, DUMP>(m, k);
+    const uint32_t x = m.U[0] ^ m.U[1] ^ m.U[2];
+    const uint32_t y = (m.U[0] & m.U[1]) | (m.U[2] & (m.U[0] | m.U[1]));
+    return __popc(x) + 2 * __popc(y);
 }
 
 template <int A, int J, bool DUMP, bool TRACK>
@@ -675,18 +673,16 @@ __device__ __forceinline__ uint32_t rstep(LaneR<S> &m, int k)
     constexpr uint32_t WB = T.shift & 31;
     const uint32_t *src = T.src ? m.wb[k] : m.wa[k];
     const uint32_t S_ = __funnelshift_l(src[-(WA + 1)], src[-WA], WB);
-    const uint32_t nw = m.U[k] & S_;
-    m.U[k] ^= nw;
-    const uint32_t c = __popc(nw);
     if constexpr (DUMP) {
-        uint32_t x = nw;
+        uint32_t x = m.U[k] & S_;
         while (x) {
             const int b = __ffs(x) - 1;
             x &= x - 1;
             m.dump[k][3 * b] = P;
         }
     }
-    return c;
+    m.U[k] &= ~S_;
+    return __popc(m.U[k]);
 }
 
 template <int A, int J, int S, bool DUMP>
@@ -747,7 +743,7 @@ __device__ __forceinline__ void phase2(Lane6 &m, uint32_t *h, int lane)
 // that block can raise this warp's running maximum best_p
 template <int A>
 __device__ __forceinline__ void replay_key(const Lane6 &m, uint64_t u, const VerifyArgs &a,
-                                           uint32_t &best_p, Acc &acc)
+                                           uint32_t &best_p, VAcc &acc)
 {
     const uint32_t bstar = __reduce_max_sync(FULL, m.lb);
     if (bstar == 0) return;
@@ -768,12 +764,12 @@ __device__ __forceinline__ void replay_key(const Lane6 &m, uint64_t u, const Ver
         if (nw) { lp = p; lbits = nw; }
     }
     const uint64_t n = 6 * (u * 32 + (uint64_t)(__ffs(lbits) - 1)) + A;
-    note_key(acc, lp, n, a.origin);
+    vnote_key(acc, lp, n, a.origin);
 }
 
 template <int A>
 __device__ __forceinline__ void replay_key_q(const LaneQ &m, uint64_t u0w, const VerifyArgs &a, uint32_t &best_p,
-                                             Acc &acc)
+                                             VAcc &acc)
 {
     uint32_t mx = 0;
 #pragma unroll
@@ -799,13 +795,13 @@ __device__ __forceinline__ void replay_key_q(const LaneQ &m, uint64_t u0w, const
             if (nw) { lp = p; lbits = nw; }
         }
         const uint64_t n = 6 * ((u0w + 32 * k) * 32 + (uint64_t)(__ffs(lbits) - 1)) + A;
-        note_key(acc, lp, n, a.origin);
+        vnote_key(acc, lp, n, a.origin);
     }
 }
 
 template <int A, int S>
 __device__ __forceinline__ void replay_key_r(const LaneR<S> &m, uint64_t u0, const VerifyArgs &a, uint32_t &best_p,
-                                             Acc &acc)
+                                             VAcc &acc)
 {
     uint32_t mx = 0;
 #pragma unroll
@@ -831,7 +827,7 @@ __device__ __forceinline__ void replay_key_r(const LaneR<S> &m, uint64_t u0, con
             if (nw) { lp = p; lbits = nw; }
         }
         const uint64_t n = 6 * ((u0 + m.li[k]) * 32 + (uint64_t)(__ffs(lbits) - 1)) + A;
-        note_key(acc, lp, n, a.origin);
+        vnote_key(acc, lp, n, a.origin);
     }
 }
 
@@ -840,7 +836,7 @@ __device__ __forceinline__ void replay_key_r(const LaneR<S> &m, uint64_t u0, con
 template <int A, bool DUMP>
 __device__ __forceinline__ void finish_word(uint32_t U, uint32_t j0, const uint32_t *wa,
                                             const uint32_t *wb, uint64_t u, uint32_t *sh_hist,
-                                            const VerifyArgs &a, Acc &acc, int lane)
+                                            const VerifyArgs &a, VAcc &acc, int lane)
 {
     uint32_t lastp = 0, lastb = 0;
     for (uint32_t j = j0; j < a.n_cand; ++j) {
@@ -855,7 +851,7 @@ __device__ __forceinline__ void finish_word(uint32_t U, uint32_t j0, const uint3
         const uint32_t c = __popc(nw);
         if (nw) {
             U ^= nw;
-            acc.sum += (uint64_t)c * p;
+            atomicAdd(&acc.c->sum, (unsigned long long)c * p);
             lastp = p; lastb = nw;
             if (DUMP) {
                 uint32_t x = nw;
@@ -871,9 +867,9 @@ __device__ __forceinline__ void finish_word(uint32_t U, uint32_t j0, const uint3
     }
     if (lastp) {
         const uint64_t n = 6 * (u * 32 + (uint64_t)(__ffs(lastb) - 1)) + A;
-        note_key(acc, lastp, n, a.origin);
+        vnote_key(acc, lastp, n, a.origin);
     }
-    acc.fast_unres += __popc(U);
+    if (U) atomicAdd(&acc.c->fast_unres, (unsigned long long)__popc(U));
     while (true) {
         const uint32_t m = __ballot_sync(FULL, U != 0);
         if (!m) break;
@@ -886,13 +882,13 @@ __device__ __forceinline__ void finish_word(uint32_t U, uint32_t j0, const uint3
         if (lane == L) {
             U &= ~(1u << bit);
             if (p) {
-                acc.sum += p;
+                atomicAdd(&acc.c->sum, (unsigned long long)p);
                 hist_add(sh_hist, a.result, bin_of_prime(p, a.sp.primes, a.n_base), 1);
-                note_key(acc, p, n, a.origin);
+                vnote_key(acc, p, n, a.origin);
             } else {
-                acc.unres += 1;
+                atomicAdd(&acc.c->unres, 1ull);
                 hist_add(sh_hist, a.result, 0, 1);
-                if (n < acc.first_unres) acc.first_unres = n;
+                atomicMin(&acc.c->first_unres, (unsigned long long)n);
             }
             if (DUMP) a.dump[(n - a.lo_e) / 2] = (uint32_t)p;
         }
@@ -913,21 +909,21 @@ __device__ __forceinline__ uint32_t valid_mask(uint64_t u, const VerifyArgs &a)
 // m = 1): p_min = 3 with q = 3, the one partner the wheel windows do not hold
 template <int A, bool DUMP>
 __device__ __forceinline__ uint32_t take_special(uint32_t U, uint64_t u, uint32_t *sh_hist,
-                                                 const VerifyArgs &a, Acc &acc)
+                                                 const VerifyArgs &a, VAcc &acc)
 {
     if (u != 0) return U;
     if (A == 4 && (U & 1u)) {
         U &= ~1u;
-        acc.sum += 2;
+        atomicAdd(&acc.c->sum, 2ull);
         atomicAdd(sh_hist + 1, 1u);
-        note_key(acc, 2, 4, a.origin);
+        vnote_key(acc, 2, 4, a.origin);
         if (DUMP) a.dump[(4 - a.lo_e) / 2] = 2;
     }
     if (A == 0 && (U & 2u)) {
         U &= ~2u;
-        acc.sum += 3;
+        atomicAdd(&acc.c->sum, 3ull);
         atomicAdd(sh_hist + 2, 1u);
-        note_key(acc, 3, 6, a.origin);
+        vnote_key(acc, 3, 6, a.origin);
         if (DUMP) a.dump[(6 - a.lo_e) / 2] = 3;
     }
     return U;
@@ -974,10 +970,11 @@ extern __shared__ uint32_t g_win[];
 
 struct Shared6 {
     uint32_t hist[kHistSmem];          // bins by prime index (runtime loop, fallback, specials)
-    uint32_t histc[3][kK];             // unrolled candidates, by class table index
+    uint32_t histc[3][kK + 1];         // per class: [0] evens entering the table, [J + 1] = A_J (hist8)
     uint32_t next_round[2];            // per window slot
     uint32_t ns[2];
     uint32_t q_base;      // word offset of the queues in dynamic shared memory
+    CtaAcc acc;
 };
 
 __device__ __forceinline__ uint32_t *sh_qU(const Shared6 &sh, int warp)
@@ -995,7 +992,7 @@ struct ClassWork {
     // the round loop and the queue flushes; keeps the hot code small)
     static __device__ __noinline__ void batch(Shared6 &sh, uint32_t &qn, uint32_t take, uint64_t u0,
                                                  const uint32_t *wA, const uint32_t *wB, uint32_t halo,
-                                                 const VerifyArgs &a, Acc &acc, uint32_t &best_p, int lane,
+                                                 const VerifyArgs &a, VAcc &acc, uint32_t &best_p, int lane,
                                                  int warp)
     {
         const uint32_t e = qn - take;
@@ -1010,7 +1007,7 @@ struct ClassWork {
         m.U = U;
         m.lb = 0; m.lu = 0;
         m.dump_w = DUMP ? a.dump + ((int64_t)(192 * u + A) - (int64_t)a.lo_e) / 2 : nullptr;
-        phase2<A, kP1, DUMP>(m, sh.histc[A / 2], lane);
+        phase2<A, kP1, DUMP>(m, sh.histc[A / 2] + 1, lane);
         replay_key<A>(m, u, a, best_p, acc);
         constexpr uint32_t j_next = kTab[A / 2].bin[kK - 1] - 1;   // odd-list index after the table
         finish_word<A, DUMP>(m.U, j_next, m.wa, m.wb, u, sh.hist, a, acc, lane);
@@ -1020,7 +1017,7 @@ struct ClassWork {
     template <bool TRACK>
     static __device__ __forceinline__ void round_q(Shared6 &sh, uint32_t &qn, uint32_t pair, uint32_t tw,
                                                    uint64_t u0, const uint32_t *wA, const uint32_t *wB,
-                                                   uint32_t halo, const VerifyArgs &a, Acc &acc,
+                                                   uint32_t halo, const VerifyArgs &a, VAcc &acc,
                                                    uint32_t &best_p, int lane, int warp)
     {
         const uint32_t li0 = pair * 32 * kW + lane;
@@ -1039,19 +1036,29 @@ struct ClassWork {
                 m.U[k] = FULL;
                 if (TRACK) { m.lb[k] = 0; m.lu[k] = 0; }
             }
-            acc.evens += 32 * kW;
+            if (lane == 0) {                                 // evens of the round, all entering the table
+                atomicAdd(&sh.histc[A / 2][0], 32u * 32u * kW);
+                atomicAdd(&acc.c->evens, 32ull * 32ull * kW);
+            }
         } else {
+            uint32_t c = 0, e = 0;
 #pragma unroll
             for (int k = 0; k < kW; ++k) {
                 const uint32_t li = li0 + 32 * k;
                 uint32_t U = li < tw ? valid_mask<A>(u0 + li, a) : 0u;
-                acc.evens += __popc(U);
+                e += __popc(U);
                 if (k == 0) U = take_special<A, DUMP>(U, u0 + li, sh.hist, a, acc);
                 m.U[k] = U;
+                c += __popc(U);
                 if (TRACK) { m.lb[k] = 0; m.lu[k] = 0; }
             }
+            c = __reduce_add_sync(FULL, c + (e << 16));          // <= 3072 each
+            if (lane == 0 && c) {
+                atomicAdd(&sh.histc[A / 2][0], c & 0xFFFFu);
+                atomicAdd(&acc.c->evens, (unsigned long long)(c >> 16));
+            }
         }
-        phase1q<A, 0, kC1, DUMP, TRACK>(m, sh.histc[A / 2], lane);
+        phase1q<A, 0, kC1, DUMP, TRACK>(m, sh.histc[A / 2] + 1, lane);
         if (TRACK) replay_key_q<A>(m, u0 + li0, a, best_p, acc);
         // survivors of candidates [0, kC1): staged past the queue's live entries,
         // then compacted to 2 (or 1) words per lane for candidates [kC1, kP1)
@@ -1082,7 +1089,7 @@ struct ClassWork {
     template <int S, bool TRACK>
     static __device__ __forceinline__ void stage(Shared6 &sh, uint32_t &qn, uint32_t e0, uint32_t cnt, uint64_t u0,
                                                  const uint32_t *wA, const uint32_t *wB, uint32_t halo,
-                                                 const VerifyArgs &a, Acc &acc, uint32_t &best_p, int lane, int warp)
+                                                 const VerifyArgs &a, VAcc &acc, uint32_t &best_p, int lane, int warp)
     {
         LaneR<S> m;
 #pragma unroll
@@ -1098,7 +1105,7 @@ struct ClassWork {
             if (DUMP) m.dump[k] = a.dump + ((int64_t)(192 * (u0 + li) + A) - (int64_t)a.lo_e) / 2;
         }
         __syncwarp();                          // staged entries read before any append
-        phase1r<A, kC1, S, DUMP, TRACK>(m, sh.histc[A / 2], lane);
+        phase1r<A, kC1, S, DUMP, TRACK>(m, sh.histc[A / 2] + 1, lane);
         if (TRACK) replay_key_r<A, S>(m, u0, a, best_p, acc);
 #pragma unroll
         for (int k = 0; k < S; ++k) {
@@ -1115,7 +1122,7 @@ struct ClassWork {
 
     static __device__ __forceinline__ void round(Shared6 &sh, uint32_t &qn, uint32_t pair, uint32_t tw,
                                                  uint64_t u0, const uint32_t *wA, const uint32_t *wB,
-                                                 uint32_t halo, const VerifyArgs &a, Acc &acc,
+                                                 uint32_t halo, const VerifyArgs &a, VAcc &acc,
                                                  uint32_t &best_p, int lane, int warp)
     {
         if constexpr (UNROLL) {
@@ -1132,7 +1139,8 @@ struct ClassWork {
                 const uint32_t li = li0 + 32 * k;
                 const uint64_t u = u0 + li;
                 uint32_t U = li < tw ? valid_mask<A>(u, a) : 0u;
-                acc.evens += __popc(U);
+                const uint32_t e = __reduce_add_sync(FULL, __popc(U));
+                if (lane == 0 && e) atomicAdd(&acc.c->evens, (unsigned long long)e);
                 if (k == 0) U = take_special<A, DUMP>(U, u, sh.hist, a, acc);
                 finish_word<A, DUMP>(U, 0, wA + halo + li, wB + halo + li, u, sh.hist, a, acc, lane);
             }
@@ -1142,7 +1150,7 @@ struct ClassWork {
 
 template <bool DUMP, bool UNROLL>
 __device__ __forceinline__ void flush_queue(int cls, Shared6 &sh, uint32_t &qn, uint64_t u0, const uint32_t *wA,
-                                            const uint32_t *wB, uint32_t halo, const VerifyArgs &a, Acc &acc,
+                                            const uint32_t *wB, uint32_t halo, const VerifyArgs &a, VAcc &acc,
                                             uint32_t &best_p, int lane, int warp)
 {
     if (!UNROLL || qn == 0) return;
@@ -1157,7 +1165,7 @@ __device__ __forceinline__ void flush_queue(int cls, Shared6 &sh, uint32_t &qn, 
 template <bool DUMP, bool UNROLL>
 __device__ __forceinline__ void mark_tile(Shared6 &sh, uint32_t &next_round, uint64_t u0, uint32_t tw,
                                           const uint32_t *wA, const uint32_t *wB, uint32_t halo,
-                                          const VerifyArgs &a, Acc &acc, uint32_t &best_p, int lane, int qwarp)
+                                          const VerifyArgs &a, VAcc &acc, uint32_t &best_p, int lane, int qwarp)
 {
     const uint32_t r1 = (tw + 32 * kW - 1) / (32 * kW);
     uint32_t qn = 0;
@@ -1183,7 +1191,7 @@ __device__ __forceinline__ void mark_tile(Shared6 &sh, uint32_t &next_round, uin
 // shared histograms -> result vector (all threads; callers barrier around it).  The
 // unrolled candidates' counts also give their share of sum p_min (count x p): the
 // marking loops keep no per-word sums (every other path adds to acc.sum directly).
-__device__ __forceinline__ void flush_hist(Shared6 &sh, const VerifyArgs &a, Acc &acc, int tid)
+__device__ __forceinline__ void flush_hist(Shared6 &sh, const VerifyArgs &a, VAcc &acc, int tid)
 {
     unsigned long long *R = (unsigned long long *)a.result;
     for (int i = tid; i < kHistSmem; i += kThreads) {
@@ -1193,13 +1201,20 @@ __device__ __forceinline__ void flush_hist(Shared6 &sh, const VerifyArgs &a, Acc
             sh.hist[i] = 0;
         }
     }
-    for (int i = tid; i < 3 * kK; i += kThreads) {
-        const uint32_t v = (&sh.histc[0][0])[i];
-        if (v) {
-            acc.sum += (uint64_t)v * c_tab[i / kK].p[i % kK];
-            atomicAdd(R + GB_R_HIST + c_tab[i / kK].bin[i % kK], (unsigned long long)v);
-            (&sh.histc[0][0])[i] = 0;
-        }
+    static_assert(3 * (kK + 1) <= kThreads, "one class-table entry per thread");
+    uint32_t v = 0;
+    const int c = tid / kK, j = tid % kK;
+    if (tid < 3 * kK) v = sh.histc[c][j] - sh.histc[c][j + 1];      // A_{j-1} - A_j
+    __syncthreads();
+    if (tid < 3 * (kK + 1)) (&sh.histc[0][0])[tid] = 0;
+    uint64_t sp = 0;
+    if (v) {
+        sp = (uint64_t)v * c_tab[c].p[j];
+        atomicAdd(R + GB_R_HIST + c_tab[c].bin[j], (unsigned long long)v);
+    }
+    if (tid < 3 * kK) {                                   // warps 0..17: share of sum p_min
+        for (int o = 16; o; o >>= 1) sp += __shfl_xor_sync(FULL, sp, o);
+        if ((tid & 31) == 0 && sp) atomicAdd(&acc.c->sum, (unsigned long long)sp);
     }
 }
 
@@ -1217,8 +1232,10 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant_
     const uint32_t nw_max = halo + a.tile_words + kWinSlack;
     if (tid == 0) sh.q_base = 2 * nw_max;
     for (int i = tid; i < kHistSmem; i += kThreads) sh.hist[i] = 0;
-    for (int i = tid; i < 3 * kK; i += kThreads) (&sh.histc[0][0])[i] = 0;
-    Acc acc;
+    for (int i = tid; i < 3 * (kK + 1); i += kThreads) (&sh.histc[0][0])[i] = 0;
+    if (tid == 0) sh.acc = CtaAcc{0, 0, 0, 0, 0, ~0ull};
+    VAcc acc;
+    acc.c = &sh.acc;
     uint32_t best_p = 0;                       // per warp: replay only blocks that can raise the max
     // contiguous run of tiles per CTA, so the sieve can carry its offsets
     const uint64_t t_begin = (uint64_t)blockIdx.x * a.n_tiles / gridDim.x;
@@ -1260,9 +1277,22 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant_
         __syncthreads();
         flush_hist(sh, a, acc, tid);
     }
-    acc.verified = acc.evens - acc.unres;
-
-    flush_acc(acc, a.result, lane);
+    // the CTA's counts (thread 0) and the max key (one atomic per warp)
+    __syncthreads();
+    unsigned long long *R = (unsigned long long *)a.result;
+    if (tid == 0) {
+        const CtaAcc c = sh.acc;
+        if (c.evens) atomicAdd(R + GB_R_EVENS, c.evens);
+        if (c.evens - c.unres) atomicAdd(R + GB_R_VERIFIED, c.evens - c.unres);
+        if (c.fast_unres) atomicAdd(R + GB_R_FASTPATH_UNRESOLVED, c.fast_unres);
+        if (c.unres) atomicAdd(R + GB_R_UNRESOLVED, c.unres);
+        if (c.sum) atomicAdd(R + GB_R_SUM_PMIN, c.sum);
+        if (c.praw) atomicMax(R + GB_R_MAX_PMIN_RAW, c.praw);
+        if (c.first_unres != ~0ull) atomicMin(R + GB_R_FIRST_UNRESOLVED_N, c.first_unres);
+    }
+    uint64_t ky = acc.key;
+    for (int o = 16; o; o >>= 1) { const uint64_t w = __shfl_xor_sync(FULL, ky, o); ky = w > ky ? w : ky; }
+    if (lane == 0 && ky) atomicMax(R + GB_R_MAX_KEY, (unsigned long long)ky);
 }
 
 
