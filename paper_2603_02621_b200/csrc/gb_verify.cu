@@ -482,24 +482,32 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
 }
 
 // ---------------------------------------------------------------------------
-// accumulators of the verify kernel: every count in per-CTA shared memory (shared
-// atomics: once per round for the evens, per tile for the histogram share of
-// sum p_min, else only on the cold paths), the max key per thread in registers --
-// the hot marking loops hold no accumulator registers
+// accumulators of the verify kernel: per-CTA, in shared memory (shared atomics:
+// once per round for the evens, per tile for the histogram share of sum p_min,
+// else only on the cold paths) -- the marking loops hold no accumulator registers
+// and pass no accumulator by reference to the out-of-line phase-2 batches
 // ---------------------------------------------------------------------------
 struct CtaAcc {
     unsigned long long evens, fast_unres, unres, sum, praw, first_unres;
-};
-struct VAcc {
-    uint64_t key = 0;          // largest make_key(p_min, n) this thread saw
-    CtaAcc *c;
+    unsigned long long key;    // largest make_key(p_min, n)
 };
 
-__device__ __forceinline__ void vnote_key(VAcc &acc, uint64_t p, uint64_t n, uint64_t origin)
+// one lane's (p, n) max-key candidate (p = 0: none); the whole warp calls it
+__device__ __forceinline__ void warp_note_key(CtaAcc *acc, uint64_t p, uint64_t n, uint64_t origin, int lane)
 {
-    const uint64_t key = make_key(p, n, origin);
-    if (key > acc.key) acc.key = key;
-    if (p >= GB_KEY_PMAX) atomicMax(&acc.c->praw, (unsigned long long)p);
+    const uint64_t key = p ? make_key(p, n, origin) : 0;
+    const uint32_t hi = __reduce_max_sync(FULL, (uint32_t)(key >> 32));
+    const uint32_t lo = __reduce_max_sync(FULL, (uint32_t)(key >> 32) == hi ? (uint32_t)key : 0u);
+    const uint64_t k = ((uint64_t)hi << 32) | lo;
+    if (lane == 0 && k) atomicMax(&acc->key, (unsigned long long)k);
+    if (p >= GB_KEY_PMAX) atomicMax(&acc->praw, (unsigned long long)p);
+}
+
+// a single lane's note (cold paths: specials, fallback)
+__device__ __forceinline__ void lane_note_key(CtaAcc *acc, uint64_t p, uint64_t n, uint64_t origin)
+{
+    atomicMax(&acc->key, (unsigned long long)make_key(p, n, origin));
+    if (p >= GB_KEY_PMAX) atomicMax(&acc->praw, (unsigned long long)p);
 }
 
 // ---------------------------------------------------------------------------
@@ -743,7 +751,7 @@ __device__ __forceinline__ void phase2(Lane6 &m, uint32_t *h, int lane)
 // that block can raise this warp's running maximum best_p
 template <int A>
 __device__ __forceinline__ void replay_key(const Lane6 &m, uint64_t u, const VerifyArgs &a,
-                                           uint32_t &best_p, VAcc &acc)
+                                           uint32_t &best_p, CtaAcc *acc)
 {
     const uint32_t bstar = __reduce_max_sync(FULL, m.lb);
     if (bstar == 0) return;
@@ -751,25 +759,27 @@ __device__ __forceinline__ void replay_key(const Lane6 &m, uint64_t u, const Ver
     if (T.p[8 * bstar - 1] < best_p) return;
     const uint32_t jr = (bstar - 1) * 8;
     best_p = max(best_p, T.p[jr]);
-    if (m.lb != bstar) return;
-    uint32_t x = m.lu, lp = 0, lbits = 0;
-    for (int i = 0; i < 8; ++i) {
-        const uint32_t p = T.p[jr + i];
-        const Trans t = trans(A, p);
-        const uint32_t *src = t.src ? m.wb : m.wa;
-        const int wa = (int)(t.shift >> 5);
-        const uint32_t S = __funnelshift_l(src[-wa - 1], src[-wa], t.shift & 31);
-        const uint32_t nw = x & S;
-        x ^= nw;
-        if (nw) { lp = p; lbits = nw; }
+    uint32_t lp = 0, lbits = 0;
+    if (m.lb == bstar) {
+        uint32_t x = m.lu;
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t p = T.p[jr + i];
+            const Trans t = trans(A, p);
+            const uint32_t *src = t.src ? m.wb : m.wa;
+            const int wa = (int)(t.shift >> 5);
+            const uint32_t S = __funnelshift_l(src[-wa - 1], src[-wa], t.shift & 31);
+            const uint32_t nw = x & S;
+            x ^= nw;
+            if (nw) { lp = p; lbits = nw; }
+        }
     }
-    const uint64_t n = 6 * (u * 32 + (uint64_t)(__ffs(lbits) - 1)) + A;
-    vnote_key(acc, lp, n, a.origin);
+    const uint64_t n = lp ? 6 * (u * 32 + (uint64_t)(__ffs(lbits) - 1)) + A : 0;
+    warp_note_key(acc, lp, n, a.origin, threadIdx.x & 31);
 }
 
 template <int A>
 __device__ __forceinline__ void replay_key_q(const LaneQ &m, uint64_t u0w, const VerifyArgs &a, uint32_t &best_p,
-                                             VAcc &acc)
+                                             CtaAcc *acc)
 {
     uint32_t mx = 0;
 #pragma unroll
@@ -780,6 +790,8 @@ __device__ __forceinline__ void replay_key_q(const LaneQ &m, uint64_t u0w, const
     if (T.p[8 * bstar - 1] < best_p) return;
     const uint32_t jr = (bstar - 1) * 8;
     best_p = max(best_p, T.p[jr]);
+    uint32_t bp = 0;
+    uint64_t bn = 0;
 #pragma unroll
     for (int k = 0; k < kW; ++k) {
         if (m.lb[k] != bstar) continue;
@@ -795,13 +807,14 @@ __device__ __forceinline__ void replay_key_q(const LaneQ &m, uint64_t u0w, const
             if (nw) { lp = p; lbits = nw; }
         }
         const uint64_t n = 6 * ((u0w + 32 * k) * 32 + (uint64_t)(__ffs(lbits) - 1)) + A;
-        vnote_key(acc, lp, n, a.origin);
+        if (lp > bp || (lp == bp && n < bn)) { bp = lp; bn = n; }
     }
+    warp_note_key(acc, bp, bn, a.origin, threadIdx.x & 31);
 }
 
 template <int A, int S>
 __device__ __forceinline__ void replay_key_r(const LaneR<S> &m, uint64_t u0, const VerifyArgs &a, uint32_t &best_p,
-                                             VAcc &acc)
+                                             CtaAcc *acc)
 {
     uint32_t mx = 0;
 #pragma unroll
@@ -812,6 +825,8 @@ __device__ __forceinline__ void replay_key_r(const LaneR<S> &m, uint64_t u0, con
     if (T.p[8 * bstar - 1] < best_p) return;
     const uint32_t jr = (bstar - 1) * 8;
     best_p = max(best_p, T.p[jr]);
+    uint32_t bp = 0;
+    uint64_t bn = 0;
 #pragma unroll
     for (int k = 0; k < S; ++k) {
         if (m.lb[k] != bstar) continue;
@@ -827,8 +842,9 @@ __device__ __forceinline__ void replay_key_r(const LaneR<S> &m, uint64_t u0, con
             if (nw) { lp = p; lbits = nw; }
         }
         const uint64_t n = 6 * ((u0 + m.li[k]) * 32 + (uint64_t)(__ffs(lbits) - 1)) + A;
-        vnote_key(acc, lp, n, a.origin);
+        if (lp > bp || (lp == bp && n < bn)) { bp = lp; bn = n; }
     }
+    warp_note_key(acc, bp, bn, a.origin, threadIdx.x & 31);
 }
 
 // candidates past the unrolled tables (runtime loop over the resident list, class
@@ -836,7 +852,7 @@ __device__ __forceinline__ void replay_key_r(const LaneR<S> &m, uint64_t u0, con
 template <int A, bool DUMP>
 __device__ __forceinline__ void finish_word(uint32_t U, uint32_t j0, const uint32_t *wa,
                                             const uint32_t *wb, uint64_t u, uint32_t *sh_hist,
-                                            const VerifyArgs &a, VAcc &acc, int lane)
+                                            const VerifyArgs &a, CtaAcc *acc, int lane)
 {
     uint32_t lastp = 0, lastb = 0;
     for (uint32_t j = j0; j < a.n_cand; ++j) {
@@ -851,7 +867,7 @@ __device__ __forceinline__ void finish_word(uint32_t U, uint32_t j0, const uint3
         const uint32_t c = __popc(nw);
         if (nw) {
             U ^= nw;
-            atomicAdd(&acc.c->sum, (unsigned long long)c * p);
+            atomicAdd(&acc->sum, (unsigned long long)c * p);
             lastp = p; lastb = nw;
             if (DUMP) {
                 uint32_t x = nw;
@@ -865,11 +881,8 @@ __device__ __forceinline__ void finish_word(uint32_t U, uint32_t j0, const uint3
         const uint32_t tot = __reduce_add_sync(FULL, c);
         if (lane == 0 && tot) hist_add(sh_hist, a.result, j + 2, tot);
     }
-    if (lastp) {
-        const uint64_t n = 6 * (u * 32 + (uint64_t)(__ffs(lastb) - 1)) + A;
-        vnote_key(acc, lastp, n, a.origin);
-    }
-    if (U) atomicAdd(&acc.c->fast_unres, (unsigned long long)__popc(U));
+    warp_note_key(acc, lastp, lastp ? 6 * (u * 32 + (uint64_t)(__ffs(lastb) - 1)) + A : 0, a.origin, lane);
+    if (U) atomicAdd(&acc->fast_unres, (unsigned long long)__popc(U));
     while (true) {
         const uint32_t m = __ballot_sync(FULL, U != 0);
         if (!m) break;
@@ -882,13 +895,13 @@ __device__ __forceinline__ void finish_word(uint32_t U, uint32_t j0, const uint3
         if (lane == L) {
             U &= ~(1u << bit);
             if (p) {
-                atomicAdd(&acc.c->sum, (unsigned long long)p);
+                atomicAdd(&acc->sum, (unsigned long long)p);
                 hist_add(sh_hist, a.result, bin_of_prime(p, a.sp.primes, a.n_base), 1);
-                vnote_key(acc, p, n, a.origin);
+                lane_note_key(acc, p, n, a.origin);
             } else {
-                atomicAdd(&acc.c->unres, 1ull);
+                atomicAdd(&acc->unres, 1ull);
                 hist_add(sh_hist, a.result, 0, 1);
-                atomicMin(&acc.c->first_unres, (unsigned long long)n);
+                atomicMin(&acc->first_unres, (unsigned long long)n);
             }
             if (DUMP) a.dump[(n - a.lo_e) / 2] = (uint32_t)p;
         }
@@ -909,21 +922,21 @@ __device__ __forceinline__ uint32_t valid_mask(uint64_t u, const VerifyArgs &a)
 // m = 1): p_min = 3 with q = 3, the one partner the wheel windows do not hold
 template <int A, bool DUMP>
 __device__ __forceinline__ uint32_t take_special(uint32_t U, uint64_t u, uint32_t *sh_hist,
-                                                 const VerifyArgs &a, VAcc &acc)
+                                                 const VerifyArgs &a, CtaAcc *acc)
 {
     if (u != 0) return U;
     if (A == 4 && (U & 1u)) {
         U &= ~1u;
-        atomicAdd(&acc.c->sum, 2ull);
+        atomicAdd(&acc->sum, 2ull);
         atomicAdd(sh_hist + 1, 1u);
-        vnote_key(acc, 2, 4, a.origin);
+        lane_note_key(acc, 2, 4, a.origin);
         if (DUMP) a.dump[(4 - a.lo_e) / 2] = 2;
     }
     if (A == 0 && (U & 2u)) {
         U &= ~2u;
-        atomicAdd(&acc.c->sum, 3ull);
+        atomicAdd(&acc->sum, 3ull);
         atomicAdd(sh_hist + 2, 1u);
-        vnote_key(acc, 3, 6, a.origin);
+        lane_note_key(acc, 3, 6, a.origin);
         if (DUMP) a.dump[(6 - a.lo_e) / 2] = 3;
     }
     return U;
@@ -990,16 +1003,18 @@ template <int A, bool DUMP, bool UNROLL>
 struct ClassWork {
     // one phase-2 batch of `take` queued words of class A (out of line: called from
     // the round loop and the queue flushes; keeps the hot code small)
-    static __device__ __noinline__ void batch(Shared6 &sh, uint32_t &qn, uint32_t take, uint64_t u0,
-                                                 const uint32_t *wA, const uint32_t *wB, uint32_t halo,
-                                                 const VerifyArgs &a, VAcc &acc, uint32_t &best_p, int lane,
-                                                 int warp)
+    // (everything by value: no local-memory round trip of the caller's state; the
+    // queue entries [qn - take, qn) are consumed, the caller lowers qn; returns the
+    // updated running max best_p)
+    static __device__ __noinline__ uint32_t batch(Shared6 &sh, uint32_t qn, uint32_t take, uint64_t u0,
+                                                  const uint32_t *wA, const uint32_t *wB, uint32_t halo,
+                                                  const VerifyArgs &a, CtaAcc *acc, uint32_t best_p, int lane,
+                                                  int warp)
     {
         const uint32_t e = qn - take;
         uint32_t li = 0, U = 0;
         if ((uint32_t)lane < take) { li = sh_qli(sh, warp)[e + lane]; U = sh_qU(sh, warp)[e + lane]; }
         __syncwarp();
-        qn = e;
         const uint64_t u = u0 + li;
         Lane6 m;
         m.wa = wA + halo + li;
@@ -1011,13 +1026,14 @@ struct ClassWork {
         replay_key<A>(m, u, a, best_p, acc);
         constexpr uint32_t j_next = kTab[A / 2].bin[kK - 1] - 1;   // odd-list index after the table
         finish_word<A, DUMP>(m.U, j_next, m.wa, m.wb, u, sh.hist, a, acc, lane);
+        return best_p;
     }
 
     // one phase-1 round: words pair*32kW + 32k + lane (k < kW) of class A
     template <bool TRACK>
     static __device__ __forceinline__ void round_q(Shared6 &sh, uint32_t &qn, uint32_t pair, uint32_t tw,
                                                    uint64_t u0, const uint32_t *wA, const uint32_t *wB,
-                                                   uint32_t halo, const VerifyArgs &a, VAcc &acc,
+                                                   uint32_t halo, const VerifyArgs &a, CtaAcc *acc,
                                                    uint32_t &best_p, int lane, int warp)
     {
         const uint32_t li0 = pair * 32 * kW + lane;
@@ -1038,7 +1054,7 @@ struct ClassWork {
             }
             if (lane == 0) {                                 // evens of the round, all entering the table
                 atomicAdd(&sh.histc[A / 2][0], 32u * 32u * kW);
-                atomicAdd(&acc.c->evens, 32ull * 32ull * kW);
+                atomicAdd(&acc->evens, 32ull * 32ull * kW);
             }
         } else {
             uint32_t c = 0, e = 0;
@@ -1055,7 +1071,7 @@ struct ClassWork {
             c = __reduce_add_sync(FULL, c + (e << 16));          // <= 3072 each
             if (lane == 0 && c) {
                 atomicAdd(&sh.histc[A / 2][0], c & 0xFFFFu);
-                atomicAdd(&acc.c->evens, (unsigned long long)(c >> 16));
+                atomicAdd(&acc->evens, (unsigned long long)(c >> 16));
             }
         }
         phase1q<A, 0, kC1, DUMP, TRACK>(m, sh.histc[A / 2] + 1, lane);
@@ -1080,7 +1096,10 @@ struct ClassWork {
             if (cnt > 32) stage<2, TRACK>(sh, qn, q0 + base, cnt, u0, wA, wB, halo, a, acc, best_p, lane, warp);
             else stage<1, TRACK>(sh, qn, q0 + base, cnt, u0, wA, wB, halo, a, acc, best_p, lane, warp);
         }
-        while (qn >= 32) batch(sh, qn, 32, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+        while (qn >= 32) {
+            best_p = batch(sh, qn, 32, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+            qn -= 32;
+        }
     }
 
     // candidates [kC1, kP1) for cnt staged words at queue entries e0.. (S per lane);
@@ -1089,7 +1108,7 @@ struct ClassWork {
     template <int S, bool TRACK>
     static __device__ __forceinline__ void stage(Shared6 &sh, uint32_t &qn, uint32_t e0, uint32_t cnt, uint64_t u0,
                                                  const uint32_t *wA, const uint32_t *wB, uint32_t halo,
-                                                 const VerifyArgs &a, VAcc &acc, uint32_t &best_p, int lane, int warp)
+                                                 const VerifyArgs &a, CtaAcc *acc, uint32_t &best_p, int lane, int warp)
     {
         LaneR<S> m;
 #pragma unroll
@@ -1122,7 +1141,7 @@ struct ClassWork {
 
     static __device__ __forceinline__ void round(Shared6 &sh, uint32_t &qn, uint32_t pair, uint32_t tw,
                                                  uint64_t u0, const uint32_t *wA, const uint32_t *wB,
-                                                 uint32_t halo, const VerifyArgs &a, VAcc &acc,
+                                                 uint32_t halo, const VerifyArgs &a, CtaAcc *acc,
                                                  uint32_t &best_p, int lane, int warp)
     {
         if constexpr (UNROLL) {
@@ -1140,7 +1159,7 @@ struct ClassWork {
                 const uint64_t u = u0 + li;
                 uint32_t U = li < tw ? valid_mask<A>(u, a) : 0u;
                 const uint32_t e = __reduce_add_sync(FULL, __popc(U));
-                if (lane == 0 && e) atomicAdd(&acc.c->evens, (unsigned long long)e);
+                if (lane == 0 && e) atomicAdd(&acc->evens, (unsigned long long)e);
                 if (k == 0) U = take_special<A, DUMP>(U, u, sh.hist, a, acc);
                 finish_word<A, DUMP>(U, 0, wA + halo + li, wB + halo + li, u, sh.hist, a, acc, lane);
             }
@@ -1150,13 +1169,14 @@ struct ClassWork {
 
 template <bool DUMP, bool UNROLL>
 __device__ __forceinline__ void flush_queue(int cls, Shared6 &sh, uint32_t &qn, uint64_t u0, const uint32_t *wA,
-                                            const uint32_t *wB, uint32_t halo, const VerifyArgs &a, VAcc &acc,
+                                            const uint32_t *wB, uint32_t halo, const VerifyArgs &a, CtaAcc *acc,
                                             uint32_t &best_p, int lane, int warp)
 {
     if (!UNROLL || qn == 0) return;
-    if (cls == 0) ClassWork<0, DUMP, UNROLL>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
-    else if (cls == 1) ClassWork<2, DUMP, UNROLL>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
-    else ClassWork<4, DUMP, UNROLL>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+    if (cls == 0) best_p = ClassWork<0, DUMP, UNROLL>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+    else if (cls == 1) best_p = ClassWork<2, DUMP, UNROLL>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+    else best_p = ClassWork<4, DUMP, UNROLL>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+    qn = 0;
 }
 
 // marking of one tile: rounds of 32 kW words of one class, handed out dynamically
@@ -1165,7 +1185,7 @@ __device__ __forceinline__ void flush_queue(int cls, Shared6 &sh, uint32_t &qn, 
 template <bool DUMP, bool UNROLL>
 __device__ __forceinline__ void mark_tile(Shared6 &sh, uint32_t &next_round, uint64_t u0, uint32_t tw,
                                           const uint32_t *wA, const uint32_t *wB, uint32_t halo,
-                                          const VerifyArgs &a, VAcc &acc, uint32_t &best_p, int lane, int qwarp)
+                                          const VerifyArgs &a, CtaAcc *acc, uint32_t &best_p, int lane, int qwarp)
 {
     const uint32_t r1 = (tw + 32 * kW - 1) / (32 * kW);
     uint32_t qn = 0;
@@ -1191,7 +1211,7 @@ __device__ __forceinline__ void mark_tile(Shared6 &sh, uint32_t &next_round, uin
 // shared histograms -> result vector (all threads; callers barrier around it).  The
 // unrolled candidates' counts also give their share of sum p_min (count x p): the
 // marking loops keep no per-word sums (every other path adds to acc.sum directly).
-__device__ __forceinline__ void flush_hist(Shared6 &sh, const VerifyArgs &a, VAcc &acc, int tid)
+__device__ __forceinline__ void flush_hist(Shared6 &sh, const VerifyArgs &a, CtaAcc *acc, int tid)
 {
     unsigned long long *R = (unsigned long long *)a.result;
     for (int i = tid; i < kHistSmem; i += kThreads) {
@@ -1214,7 +1234,7 @@ __device__ __forceinline__ void flush_hist(Shared6 &sh, const VerifyArgs &a, VAc
     }
     if (tid < 3 * kK) {                                   // warps 0..17: share of sum p_min
         for (int o = 16; o; o >>= 1) sp += __shfl_xor_sync(FULL, sp, o);
-        if ((tid & 31) == 0 && sp) atomicAdd(&acc.c->sum, (unsigned long long)sp);
+        if ((tid & 31) == 0 && sp) atomicAdd(&acc->sum, (unsigned long long)sp);
     }
 }
 
@@ -1233,44 +1253,47 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant_
     if (tid == 0) sh.q_base = 2 * nw_max;
     for (int i = tid; i < kHistSmem; i += kThreads) sh.hist[i] = 0;
     for (int i = tid; i < 3 * (kK + 1); i += kThreads) (&sh.histc[0][0])[i] = 0;
-    if (tid == 0) sh.acc = CtaAcc{0, 0, 0, 0, 0, ~0ull};
-    VAcc acc;
-    acc.c = &sh.acc;
+    if (tid == 0) sh.acc = CtaAcc{0, 0, 0, 0, 0, ~0ull, 0};
+    CtaAcc *const acc = &sh.acc;
     uint32_t best_p = 0;                       // per warp: replay only blocks that can raise the max
-    // contiguous run of tiles per CTA, so the sieve can carry its offsets
+    // contiguous run of tiles per CTA, so the sieve can carry its offsets.  Nothing of
+    // the sieve state stays live across the marking phase (register pressure): the
+    // carry descriptor is rebuilt per tile from the grid constants, the running
+    // steady count lives in shared memory.
     const uint64_t t_begin = (uint64_t)blockIdx.x * a.n_tiles / gridDim.x;
-    const uint64_t t_end = (uint64_t)(blockIdx.x + 1) * a.n_tiles / gridDim.x;
-    Carry6 cy;
-    cy.off = a.carry + (uint64_t)blockIdx.x * 2 * a.carry_stride;
-    cy.stride = a.carry_stride;
-    cy.n_carry = a.n_carry;
-    cy.have_prev = false;
-    cy.n_steady = 0;
-    cy.init = false;
-    cy.tile_m = 32 * a.tile_words;
-    uint32_t ns_run = 0;                       // thread 0: running steady count (monotone)
-    const MedSched med{a.med_idx, a.med_off};
+    const uint32_t n_mine = (uint32_t)((uint64_t)(blockIdx.x + 1) * a.n_tiles / gridDim.x - t_begin);
+    if (tid == 0) sh.ns[1] = 0;                // running (monotone) steady count
 
-    for (uint64_t tile = t_begin; tile < t_end; ++tile) {
-        const uint64_t u0 = a.u_first + tile * a.tile_words;
+    for (uint32_t t = 0; t < n_mine; ++t) {
+        const uint64_t u0 = a.u_first + (t_begin + t) * a.tile_words;
         const uint32_t tw = (uint32_t)min((uint64_t)a.tile_words, a.u_end - u0);
         const int64_t g0 = (int64_t)u0 - (int64_t)halo;
         uint32_t *wA = win, *wB = win + nw_max;
         __syncthreads();                      // previous tile fully consumed
-        if (tid == 0) {
-            sh.next_round[0] = 0;
-            sh.ns[0] = steady_count(cy, g0, a.sp, ns_run);
+        {
+            Carry6 cy;
+            cy.off = a.carry + (uint64_t)blockIdx.x * 2 * a.carry_stride;
+            cy.stride = a.carry_stride;
+            cy.n_carry = a.n_carry;
+            cy.have_prev = t > 0;
+            cy.tile_m = 32 * a.tile_words;
+            if (tid == 0) {
+                sh.next_round[0] = 0;
+                uint32_t ns_run = sh.ns[1];
+                sh.ns[0] = steady_count(cy, g0, a.sp, ns_run);
+                sh.ns[1] = ns_run;
+            }
+            __syncthreads();
+            cy.n_steady = sh.ns[0] & 0x7FFFFFFFu;
+            cy.init = sh.ns[0] >> 31;
+            const MedSched med{a.med_idx, a.med_off};
+            if (cy.tile_m == kTileM)
+                sieve6_window<true>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask, a.lmask_g0,
+                                    a.lmask_stride, tid);
+            else
+                sieve6_window<false>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask, a.lmask_g0,
+                                     a.lmask_stride, tid);
         }
-        __syncthreads();
-        cy.n_steady = sh.ns[0] & 0x7FFFFFFFu;
-        cy.init = sh.ns[0] >> 31;
-        if (cy.tile_m == kTileM)
-            sieve6_window<true>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask, a.lmask_g0,
-                                a.lmask_stride, tid);
-        else
-            sieve6_window<false>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask, a.lmask_g0,
-                                 a.lmask_stride, tid);
-        cy.have_prev = true;
         __syncthreads();
         mark_tile<DUMP, UNROLL>(sh, sh.next_round[0], u0, tw, wA, wB, halo, a, acc, best_p, lane, warp);
         // per-tile flush of the shared histograms keeps their 32-bit bins exact
@@ -1289,10 +1312,8 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant_
         if (c.sum) atomicAdd(R + GB_R_SUM_PMIN, c.sum);
         if (c.praw) atomicMax(R + GB_R_MAX_PMIN_RAW, c.praw);
         if (c.first_unres != ~0ull) atomicMin(R + GB_R_FIRST_UNRESOLVED_N, c.first_unres);
+        if (c.key) atomicMax(R + GB_R_MAX_KEY, c.key);
     }
-    uint64_t ky = acc.key;
-    for (int o = 16; o; o >>= 1) { const uint64_t w = __shfl_xor_sync(FULL, ky, o); ky = w > ky ? w : ky; }
-    if (lane == 0 && ky) atomicMax(R + GB_R_MAX_KEY, (unsigned long long)ky);
 }
 
 
