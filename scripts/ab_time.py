@@ -18,13 +18,14 @@ ap.add_argument("--span", type=int, default=36)
 ap.add_argument("--N", default="1e12")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--rounds", type=int, default=2)
+ap.add_argument("--hi", default=None, help="exclusive top of the range (e.g. 4000000000000000000 for C5)")
 a = ap.parse_args()
 libs = [os.path.join(ROOT, "paper_2603_02621_b200", "libgb.so")] + sorted(glob.glob(os.path.join(ROOT, "ab", "*.so")))
 for rnd in range(a.rounds):
     for lib in libs:
         env = dict(os.environ, GB_LIB=lib)
         r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "prof_one.py"), "--span", str(a.span),
-                            "--N", a.N, "--time", str(a.reps)], env=env, capture_output=True, text=True)
+                            "--N", a.N, "--time", str(a.reps)] + (["--hi", a.hi] if a.hi else []), env=env, capture_output=True, text=True)
         lines = [l for l in r.stdout.splitlines() if l.startswith("{") or l.startswith("TIME")]
         print(os.path.basename(lib), r.returncode, " | ".join(lines), r.stderr[-300:] if r.returncode else "",
               flush=True)
