@@ -57,10 +57,13 @@ def parse():
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--N", type=float, default=None, help="custom range [4, N] (overrides --workload)")
     ap.add_argument("--p-max", type=int, default=65521)
-    ap.add_argument("--mode", default="bulk", choices=["bulk", "pern", "resident"],
+    ap.add_argument("--mode", default="bulk", choices=["bulk", "pern", "resident", "counts"],
                     help="bulk: the product path (inverted bulk marking); pern: the paper's per-n "
                          "gpu3 kernel (NEXT-1, PAPER.md:82-95); resident: the paper's gpu2 with the "
-                         "whole odd bitset of [3, hi) sieved into HBM each step (NEXT-2, PAPER.md:41-59)")
+                         "whole odd bitset of [3, hi) sieved into HBM each step (NEXT-2, PAPER.md:41-59); "
+                         "counts: Goldbach partition counts c(n) of the top --counts-window even n below N "
+                         "(default N = 1e9; NEXT-4, PAPER.md:421)")
+    ap.add_argument("--counts-window", type=int, default=16384, help="even n per step in --mode counts")
     ap.add_argument("--strips-per-rank", type=int, default=None,
                     help="default 8 (balances the growth of work with n); 2 for c5 (the window's cost "
                          "is flat; fewer partial K-LARGE chunks)")
@@ -228,16 +231,15 @@ def load_peaks():
     return peaks, pint
 
 
-def ncu_traffic(kernel: str, tag: str, mode: str):
-    """DRAM read+write bytes per even n of `kernel` from the committed ncu --set full
-    capture of this workload (profiles/*_<kernel>_<tag>[_<mode>]_ncu.json), or None."""
+def ncu_capture(kernel: str, wl: str, mode: str):
+    """The committed ncu --set full summary of `kernel` on this workload
+    (profiles/r<NN>_<kernel>_<workload>[_<mode>].json, newest round first), or None."""
     import glob
-    suffix = f"_{tag}" + ("" if mode == "bulk" else f"_{mode}")
-    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_{kernel}{suffix}_ncu.json")))
+    suffix = f"_{wl}" + ("" if mode == "bulk" else f"_{mode}")
+    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_{kernel}{suffix}.json")))
     if not caps:
         return None, None
-    cap = json.load(open(caps[-1]))
-    return cap.get("dram_bytes_per_even"), os.path.relpath(caps[-1], ROOT)
+    return json.load(open(caps[-1])), os.path.relpath(caps[-1], ROOT)
 
 
 # ----------------------------------------------------------------- result check
@@ -267,6 +269,111 @@ def check_result(res, lo, hi, tag):
                          "no unresolved, sum hist = evens)"}
 
 
+# ----------------------------------------------------------------- NEXT-4 leg
+def run_counts(args, rank: int, world: int, local: int):
+    """Goldbach partition counts c(n) (section 4.5; R13) for the
+    top W even n of [4, N] on one GPU: one step = gb_sieve_segment of the odd bitset of
+    [3, N] + gb_partition_counts of the window.  Metric: c(n) values per second.
+    Roofline: the POPC pipe (one SHF + AND + POPC per (n, 32 i-bit word) pair, ~n/128
+    pairs per n; 16 POPC lanes/clk/SM measured, profiles/peaks_int.json).  Check: the
+    CPU oracle's plain scan (oracle.partition_counts) on 4 n of the window."""
+    import numpy as np
+    import torch
+    if world > 1 and rank != 0:
+        return                                     # single-GPU leg: no data-path collective
+    N = int(args.N) if args.N is not None else 10**9
+    W = args.counts_window
+    hi = N + 1
+    lo = hi - 2 * W
+    lo += lo & 1
+    torch.cuda.set_device(local)
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2603_02621_b200 import gb
+    from paper_2603_02621_b200.verifier import Verifier
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    V = Verifier(hi_max=hi + 128, device=local, stream=stream)
+    n_words = (hi - 3 + 127) // 128
+    bits = torch.empty(n_words, dtype=torch.int64, device=dev)
+    out = torch.empty(W, dtype=torch.int64, device=dev)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(max(4 * l2, 1 << 28) // 4, dtype=torch.int32, device=dev)
+
+    def step(ev=None):
+        gb.gb_sieve_segment(V.ctx, 0, n_words, bits, stream)
+        if ev is not None:
+            ev[0].record(stream)
+        gb.gb_partition_counts(V.ctx, lo, hi, bits, n_words, out, stream)
+        if ev is not None:
+            ev[1].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    launches0 = gb.gb_launch_count()
+    st, kt = [], []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        s0.record(stream)
+        step(k)
+        s1.record(stream)
+        st.append((s0, s1))
+        kt.append(k)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    launches = gb.gb_launch_count() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in st]
+    kern_ms = [a.elapsed_time(b) for a, b in kt]
+    value = W * args.steps / (sum(step_ms) / 1e3)
+    # e2e: the same step through the binding + D2H of the counts to pinned host memory
+    h = torch.empty(W, dtype=torch.int64).pin_memory()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(2):
+        step()
+        h.copy_(out, non_blocking=True)
+        stream.synchronize()
+    e2e_s = (time.perf_counter() - t0) / 2
+    got = out.cpu().numpy()
+    from oracle import oracle
+    picks = [0, W // 3, (2 * W) // 3, W - 1]
+    want = [int(oracle.partition_counts(lo + 2 * i, lo + 2 * i + 1)[0]) for i in picks]
+    ok = all(int(got[i]) == w for i, w in zip(picks, want))
+    pint = load_peaks()[1] or {}
+    popc = (pint.get("per_sm_lane_ops_per_clk") or {}).get("popc", 16.0)
+    sm_mhz = load_peaks()[0].get("sm_max_mhz", 1965.0)
+    peak = NSM * popc * sm_mhz * 1e6 / 1e12
+    pairs = sum(((n - 6) // 2 // 2) // 32 + 1 for n in range(lo, hi, 2))   # i-words per n (i <= K/2)
+    ach = pairs / (statistics.mean(kern_ms) / 1e3) / 1e12
+    line = {"metric": f"Goldbach partition counts c(n) per second, the top {W} even n of [4, {N:.0e}] "
+                      "(NEXT-4) [counts mode]",
+            "value": value, "unit": "c(n)/s", "n_gpus": 1, "steps": args.steps, "warmup": max(3, args.warmup),
+            "ms_per_step": statistics.mean(step_ms), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic (deterministic number-theoretic range)",
+            "config": {"workload": f"c(n) for even n in [{lo}, {hi})", "lo": lo, "hi": hi, "mode": "counts",
+                       "l2": "flushed between steps"},
+            "gpu_launches": launches, "clocks": clocks,
+            "e2e": {"value": W / e2e_s, "unit": "c(n)/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 * W,
+                    "note": "gb_sieve_segment + gb_partition_counts + D2H of the counts (pinned)"},
+            "roofline": {"bound": "popc", "achieved": ach, "peak": peak, "unit": "T popc/s", "frac": ach / peak,
+                         "kernel": "counts_kernel (popcount-AND of the odd bitset against its reversed shifts)",
+                         "ops_basis": f"{pairs / W:.4g} 32-bit i-words per n (i <= K/2, K = (n-6)/2), one POPC each",
+                         "peak_basis": f"148 SM x {popc:.2f} POPC lanes/clk x {sm_mhz:.0f} MHz (profiles/peaks_int.json)",
+                         "kernel_ms_per_launch": statistics.mean(kern_ms),
+                         "sieve_ms_per_step": statistics.mean(step_ms) - statistics.mean(kern_ms)},
+            "check": {"ok": ok, "oracle_points": {str(lo + 2 * i): w for i, w in zip(picks, want)}},
+            "step_ms": step_ms}
+    print(json.dumps(line), flush=True)
+    V.close()
+    if not ok and not args.no_check:
+        sys.exit(1)
+
+
 # ----------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -275,6 +382,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+
+    if args.mode == "counts":
+        run_counts(args, rank, world, local)
         return
 
     import numpy as np
@@ -428,7 +539,9 @@ def main():
     clears_red = recip_sum(61, sqrt_hi)            # the part not done by word patterns (p > 61)
     w_iters = mark_word_iters(hi)
     ops_per_even = clears + 6 * w_iters            # 1 op per clear, 6 per 64-bit word-iteration
-    dram_pe, dram_src = ncu_traffic("verify_kernel" if args.mode == "bulk" else "pern_kernel", tag or "", args.mode)
+    wl_key = args.workload if args.N is None else f"N{tag}"
+    cap, dram_src = ncu_capture("verify_kernel" if args.mode == "bulk" else "pern_kernel", wl_key, args.mode)
+    dram_pe = cap.get("dram_bytes_per_even") if cap else None
     if args.mode == "bulk":
         achieved = ops_per_even * evens_per_launch / avg_launch_s / 1e12
         roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Tops/s",
@@ -495,21 +608,28 @@ def main():
                               "peak_basis": f"148 SM x {red_rate:.2f} red.shared.and lanes/clk x {sm_mhz:.0f} MHz; "
                                             f"{peak_src}"}}
         del out
-    if args.mode == "bulk" and sieve_ms_per_int is not None:
-        # the fused kernel's two halves: the standalone sieve's time per integer stands
-        # for the fused sieve phase (same sieve6_window code; it also re-interleaves
-        # and writes out, so this over-states the sieve half), the rest is marking
-        span_ints = evens_per_launch * 2
-        t_sieve = sieve_ms_per_int * span_ints / 1e3
+    share = (cap or {}).get("phase_share_samples")
+    if args.mode == "bulk" and (share or sieve_ms_per_int is not None):
+        # the fused kernel's two halves: the sieve share of the kernel's stall samples in
+        # the committed ncu capture of this workload (scripts/ncu_regions.py: time per
+        # source region), else the standalone sieve's time per integer (an over-estimate:
+        # it also re-interleaves and writes out); the rest is marking
+        if share:
+            t_sieve = share.get("sieve", 0.0) * avg_launch_s
+            split_basis = f"sieve share {share.get('sieve', 0.0):.3f} of the stall samples in {dram_src}"
+        else:
+            t_sieve = sieve_ms_per_int * evens_per_launch * 2 / 1e3
+            split_basis = "standalone gb_sieve_segment time per integer x this launch's integers"
+        t_sieve = max(t_sieve, 1e-12)
         t_mark = max(avg_launch_s - t_sieve, 1e-12)
         mark_ach = 6 * w_iters * evens_per_launch / t_mark / 1e12
         sieve_ach = clears_red * evens_per_launch / t_sieve / 1e12
         roofline["sieve"] = {"bound": "smem_red", "achieved": sieve_ach, "peak": red_peak, "unit": "Tops/s",
                              "frac": sieve_ach / red_peak, "est_share_of_kernel": t_sieve / avg_launch_s,
-                             "basis": "standalone gb_sieve_segment time per integer x this launch's integers"}
+                             "basis": split_basis + f"; {clears_red:.3f} clears per even by primes > 61"}
         roofline["mark"] = {"bound": "alu", "achieved": mark_ach, "peak": alu_peak, "unit": "Tops/s",
                             "frac": mark_ach / alu_peak, "est_share_of_kernel": t_mark / avg_launch_s,
-                            "basis": "verify_kernel time minus the sieve estimate; 6 ops x SURVEY word-iterations"}
+                            "basis": "verify_kernel time minus the sieve share; 6 ops x SURVEY word-iterations"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

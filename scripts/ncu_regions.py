@@ -63,8 +63,8 @@ def region_of(starts, ln):
     return cur
 
 
-def main():
-    rep = sys.argv[1]
+def breakdown(rep):
+    """{region: {"ins", "samp", "stall": {...}}} of one capture"""
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
     starts = regions()
@@ -92,6 +92,27 @@ def main():
         for i, n in enumerate(names):
             if n.startswith("stall_") and "(Not Issued)" not in n:
                 d["stall"][n[6:]] = d["stall"].get(n[6:], 0) + num(r[i])
+    return agg
+
+
+def phase_shares(rep):
+    """share of stall samples (~ time) and of warp instructions in the sieve regions,
+    the marking regions and the rest"""
+    agg = breakdown(rep)
+    ts = sum(d["samp"] for d in agg.values()) or 1
+    ti = sum(d["ins"] for d in agg.values()) or 1
+    out = {"samples": {}, "instructions": {}}
+    for k, d in agg.items():
+        ph = "sieve" if k.startswith("sieve") else ("mark" if k.startswith("mark") or k in ("acc", "flush_hist")
+                                                     else "other")
+        out["samples"][ph] = out["samples"].get(ph, 0) + d["samp"] / ts
+        out["instructions"][ph] = out["instructions"].get(ph, 0) + d["ins"] / ti
+    return out
+
+
+def main():
+    rep = sys.argv[1]
+    agg = breakdown(rep)
     ti = sum(d["ins"] for d in agg.values()) or 1
     ts = sum(d["samp"] for d in agg.values()) or 1
     print(f"total warp instructions {ti:,}  stall samples {ts:,}")

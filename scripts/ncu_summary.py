@@ -72,6 +72,16 @@ def main():
             tot[h[6:]] += int(r[shdr.index(h)] or 0)
     T = sum(tot.values()) or 1
     res["stall_pct"] = {k: round(100 * v / T, 1) for k, v in sorted(tot.items(), key=lambda x: -x[1])[:10]}
+    if "verify_kernel" in res["kernel"]:
+        # sieve vs marking share of the kernel (stall samples ~ time), for bench.py's
+        # separate K-SIEVE / K-MARK rooflines
+        import os
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        from ncu_regions import phase_shares
+        sh = phase_shares(a.rep)
+        res["phase_share_samples"] = {k: round(v, 4) for k, v in sh["samples"].items()}
+        res["phase_share_instructions"] = {k: round(v, 4) for k, v in sh["instructions"].items()}
     if a.evens:
         res["evens"] = a.evens
         res["evens_per_s_under_ncu"] = a.evens / res["duration"]
@@ -81,9 +91,12 @@ def main():
     with open(a.out + ".md", "w") as f:
         f.write(f"# ncu summary: {res['kernel'][:80]}\n\n{a.note}\n\n| metric | value |\n|---|---|\n")
         for k, v in res.items():
-            if k in ("stall_pct", "kernel", "note", "report"):
+            if k in ("stall_pct", "kernel", "note", "report") or isinstance(v, dict):
                 continue
             f.write(f"| {k} | {v:.6g} |\n" if isinstance(v, float) else f"| {k} | {v} |\n")
+        for k in ("phase_share_samples", "phase_share_instructions"):
+            if k in res:
+                f.write(f"| {k} | " + ", ".join(f"{n} {v:.3f}" for n, v in res[k].items()) + " |\n")
         f.write("\nStall mix (% of warp-state samples): " +
                 ", ".join(f"{k} {v}" for k, v in res["stall_pct"].items()) + "\n")
     print(json.dumps(res, indent=1))
