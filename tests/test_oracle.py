@@ -297,6 +297,17 @@ def test_golden_c5_window_consistency():
     assert 4 * 10**18 - 10**11 <= g["max_pmin_n"] < 4 * 10**18
 
 
+@pytest.mark.parametrize("tag", ["1e06", "1e09", "1e10", "1e11", "1e12", "c5_4e18"])
+def test_golden_chunk_files_consistent(tag):
+    """Every per-chunk checksum file (oracle-written) has one entry per 2^24 evens of
+    its range and sums, mod 2^64, to the golden's sum n * p_min."""
+    doc = json.load(open(os.path.join(GOLDEN, f"verify_{tag}.json")))
+    chk = np.load(os.path.join(GOLDEN, doc["chunk_chk_file"]))
+    evens = doc["result"]["evens"]
+    assert chk.dtype == np.uint64 and chk.size == -(-evens // doc["chunk_evens"])
+    assert int(chk.sum(dtype=np.uint64)) == doc["result"]["chk"]
+
+
 # ---------------------------------------------------------------- c(n) (NEXT-4)
 def test_partition_counts_hand_values():
     """c(n) = #{p prime <= n/2 : n - p prime} (R13): 4 = 2+2; 10 = 3+7 = 5+5;
