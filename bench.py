@@ -609,18 +609,15 @@ def main():
                                             f"{peak_src}"}}
         del out
     share = (cap or {}).get("phase_share_samples")
-    if args.mode == "bulk" and (share or sieve_ms_per_int is not None):
+    if args.mode == "bulk" and not share:
+        roofline["split_note"] = ("no ncu capture of this workload with per-region samples in profiles/: "
+                                  "no separate K-SIEVE / K-MARK fractions")
+    if args.mode == "bulk" and share:
         # the fused kernel's two halves: the sieve share of the kernel's stall samples in
         # the committed ncu capture of this workload (scripts/ncu_regions.py: time per
-        # source region), else the standalone sieve's time per integer (an over-estimate:
-        # it also re-interleaves and writes out); the rest is marking
-        if share:
-            t_sieve = share.get("sieve", 0.0) * avg_launch_s
-            split_basis = f"sieve share {share.get('sieve', 0.0):.3f} of the stall samples in {dram_src}"
-        else:
-            t_sieve = sieve_ms_per_int * evens_per_launch * 2 / 1e3
-            split_basis = "standalone gb_sieve_segment time per integer x this launch's integers"
-        t_sieve = max(t_sieve, 1e-12)
+        # source region); the rest (marking + bookkeeping) is the marking half
+        t_sieve = max(share.get("sieve", 0.0) * avg_launch_s, 1e-12)
+        split_basis = f"sieve share {share.get('sieve', 0.0):.3f} of the stall samples in {dram_src}"
         t_mark = max(avg_launch_s - t_sieve, 1e-12)
         mark_ach = 6 * w_iters * evens_per_launch / t_mark / 1e12
         sieve_ach = clears_red * evens_per_launch / t_sieve / 1e12
