@@ -31,9 +31,8 @@ uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 constexpr uint64_t kMaxSms = 160;   // workspace sizing bound (B200: 148)
 
 struct Layout {
-    uint64_t R, bits_words, list_cap, n_blk, carry_stride, carry_ctas, lmask_stride, lcap;
-    uint64_t off_bits, off_primes, off_magic, off_tmod, off_carry, off_lmask, off_lbkt, off_lbatch, off_sched,
-        off_blk, off_counter,
+    uint64_t R, bits_words, list_cap, n_blk, carry_stride, carry_ctas, lmask_stride;
+    uint64_t off_bits, off_primes, off_magic, off_tmod, off_carry, off_lmask, off_sched, off_blk, off_counter,
         off_res, off_dump, off_seg, total;
 };
 
@@ -74,18 +73,6 @@ bool plan(uint64_t hi_max, uint32_t p_max, Layout &L)
     L.off_tmod = o;    o = align_up(o + 16 * L.list_cap, 256);
     L.off_carry = o;   o = align_up(o + 8 * L.carry_stride * (uint64_t)kMaxBlocksPerSm * kMaxSms, 256);
     L.off_lmask = o;   o = align_up(o + 8 * L.lmask_stride, 256);
-    // K-LARGE per-tile hit lists: capacity 1.3x the expected hits of a window of the
-    // largest tile (192 integers per word x 0.171 of the cofactors x sum 1/p over the
-    // primes in (2^21, R]) + slack; a fuller list spills to the mask (correct, slower)
-    L.lcap = 0;
-    if (L.lmask_stride) {
-        const double span = 192.0 * (kTileWords + verify_halo(p_max) + 1);
-        const double lnln = std::log(std::log((double)sq)) - std::log(std::log((double)kCarryPrimeMax));
-        L.lcap = align_up((uint64_t)(1.3 * span * 0.171 * std::max(lnln, 0.0)) + 8192, 32);
-    }
-    L.off_lbkt = o;    o = align_up(o + 4 * (uint64_t)kLargeTilesPerSm * kMaxSms * (L.lcap + 1) + 256, 256);
-    // K-LARGE hit-balanced batch boundaries (prime indices; >= kBucketMinBatch primes each)
-    L.off_lbatch = o;  o = align_up(o + (L.lcap ? 4 * (L.list_cap / kBucketMinBatch + 64) : 0), 256);
     L.off_sched = o;   o = align_up(o + 2 * 1024 + 4 * (kThreads / 32 + 1), 256);
     L.off_blk = o;     o = align_up(o + 8 * (L.n_blk + 1), 256);
     L.off_counter = o; o = align_up(o + 256, 256);
@@ -210,12 +197,6 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
     c->carry_stride = L.carry_stride;
     c->lmask = L.lmask_stride ? (uint32_t *)(ws + L.off_lmask) : nullptr;
     c->lmask_stride = L.lmask_stride;
-    c->lcap = (uint32_t)L.lcap;
-    c->lbkt = L.lcap ? (uint32_t *)(ws + L.off_lbkt) : nullptr;
-    c->lfill = L.lcap ? c->lbkt + (uint64_t)kLargeTilesPerSm * kMaxSms * L.lcap : nullptr;
-    c->lovf = L.lcap ? c->lfill + (uint64_t)kLargeTilesPerSm * kMaxSms : nullptr;
-    c->lbatch = L.lcap ? (uint32_t *)(ws + L.off_lbatch) : nullptr;
-    c->n_lbatch = 0;
     c->med_idx = (uint16_t *)(ws + L.off_sched);
     c->med_off = (uint32_t *)(ws + L.off_sched + 2 * 1024);
     c->blk = (uint64_t *)(ws + L.off_blk);
@@ -271,35 +252,6 @@ gb_status gb_ctx_create(gb_ctx **out, int device, uint64_t origin, uint64_t hi_m
     if (cudaMemcpy(c->h_primes.data(), c->primes, 4ull * n_base, cudaMemcpyDeviceToHost) != cudaSuccess) {
         delete c;
         return GB_ECUDA;
-    }
-    // K-LARGE bucket batches: consecutive primes > kCarryPrimeMax grouped so that each
-    // batch makes about kBucketBatchHits hits in a full chunk (a prime p makes about
-    // 0.171 x 192 x chunk words / p), so a batch's staged entries per tile stay well
-    // below kBucketStage; the producer CTAs take batches round-robin
-    if (c->lbatch) {
-        const uint32_t h0 = verify_halo(c->h_primes[count_le(c->h_primes, p_max) - 1]);
-        const double chunk_ints = 192.0 * ((double)kLargeTilesPerSm * c->num_sms * verify_tile_words(h0) + h0);
-        std::vector<uint32_t> bs;
-        uint32_t i = count_le(c->h_primes, kCarryPrimeMax);
-        bs.push_back(i);
-        double acc = 0.0;
-        uint32_t cnt = 0;
-        const uint64_t cap_b = L.list_cap / kBucketMinBatch + 63;
-        for (; i < n_base; ++i) {
-            acc += 0.171 * chunk_ints / c->h_primes[i];
-            if (++cnt >= kBucketMinBatch && (acc >= kBucketBatchHits || cnt >= kBucketMaxBatch)) {
-                bs.push_back(i + 1);
-                acc = 0.0;
-                cnt = 0;
-            }
-        }
-        if (bs.back() != n_base) bs.push_back((uint32_t)n_base);
-        if (bs.size() > cap_b) { delete c; return GB_EINTERNAL; }
-        if (cudaMemcpy(c->lbatch, bs.data(), 4 * bs.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
-            delete c;
-            return GB_ECUDA;
-        }
-        c->n_lbatch = (uint32_t)(bs.size() - 1);
     }
     // LPT schedule of the medium primes (31 < p <= kWarpPrimeMax) over the verify
     // CTA's warps, by estimated marking work (hits per full window / 32 lanes + setup)
@@ -425,7 +377,6 @@ gb_status gb_sieve_segment(gb_ctx *ctx, uint64_t word_lo, uint64_t n_words, uint
             L.nw = (uint32_t)(b.g_end - b.g_first + 1);   // + the class-A word above the last tile
             L.stride = ctx->lmask_stride;
             L.mask = ctx->lmask;
-            L.bkt = nullptr;                             // mask mode for the sieve-out path
             b.lmask = ctx->lmask;
             b.lmask_g0 = L.g0;
             b.lmask_stride = L.stride;
@@ -515,10 +466,6 @@ gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_m
     a.lmask = nullptr;
     a.lmask_g0 = 0;
     a.lmask_stride = 0;
-    a.lbkt = nullptr;
-    a.lfill = nullptr;
-    a.lcap = 0;
-    a.lovf = nullptr;
     const uint32_t i_large = count_le(ctx->h_primes, kCarryPrimeMax);
     if (a.sp.n_use <= i_large)
         return launch_verify(a, grid, smem, S(stream)) == cudaSuccess ? GB_OK : GB_ECUDA;
@@ -549,23 +496,6 @@ gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_m
         b.lmask = ctx->lmask;
         b.lmask_g0 = L.g0;
         b.lmask_stride = L.stride;
-#ifdef GB_AB_BUCKET
-        L.bkt = ctx->lbkt;
-        L.fill = ctx->lfill;
-        L.cap = ctx->lcap;
-        L.ovf = ctx->lovf;
-        L.batch = ctx->lbatch;
-        L.n_batch = ctx->n_lbatch;
-        L.tw = a.tile_words;
-        L.span = a.tile_words + a.halo;
-        L.nt = (uint32_t)nt;
-        b.lbkt = ctx->lbkt;
-        b.lfill = ctx->lfill;
-        b.lcap = ctx->lcap;
-        b.lovf = ctx->lovf;
-#else
-        L.bkt = nullptr;
-#endif
         if (launch_large(L, ctx->num_sms, S(stream)) != cudaSuccess) return GB_ECUDA;
         const int gb = (int)std::min<uint64_t>((uint64_t)grid, nt);
         if (launch_verify(b, gb, smem, S(stream)) != cudaSuccess) return GB_ECUDA;

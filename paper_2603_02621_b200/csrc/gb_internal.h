@@ -59,31 +59,7 @@ struct LargeArgs {
     uint32_t nw;
     uint64_t stride;
     uint32_t *mask;
-    // Bucket mode (gb_verify_range): the hits go to per-tile lists of window bit
-    // positions that the verify kernel applies in shared memory; the mask above only
-    // takes the hits a full list cannot hold (*ovf != 0 then).  Tile t's window is
-    // chunk words [t tw, t tw + span), span = tw + below + above, t < nt.
-    uint32_t *bkt;            // nullable: mask mode
-    uint32_t *fill;           // nt counters (entries offered per tile)
-    uint32_t cap;             // entries per tile list
-    uint32_t *ovf;            // set when some entry went to the mask
-    uint32_t tw, span, nt;
-    const uint32_t *batch;    // n_batch + 1 prime-index boundaries (hit-balanced, host-planned)
-    uint32_t n_batch;
 };
-#ifndef GB_AB_BK_THREADS
-constexpr int kBucketThreads = 1024;
-constexpr int kBucketStage = 96;          // per-tile staging entries in the producer CTA's shared memory
-constexpr double kBucketBatchHits = 16000; // expected hits per batch in a full chunk (~36 per tile of 444)
-constexpr int kBucketCtasPerSm = 1;
-#else
-constexpr int kBucketThreads = GB_AB_BK_THREADS;
-constexpr int kBucketStage = 40;
-constexpr double kBucketBatchHits = 6000;
-constexpr int kBucketCtasPerSm = 3;
-#endif
-constexpr int kBucketMinBatch = 64;       // primes per batch, at least / at most
-constexpr int kBucketMaxBatch = 65536;
 
 struct SegmentArgs {
     SievePrimes sp;
@@ -123,10 +99,6 @@ struct VerifyArgs {
     const uint32_t *lmask;    // K-LARGE mask of this chunk (nullable): ANDed into every window
     int64_t lmask_g0;         // g of mask word 0
     uint64_t lmask_stride;    // class B words start here
-    const uint32_t *lbkt;     // K-LARGE per-tile hit lists of this chunk (nullable; LargeArgs)
-    const uint32_t *lfill;
-    uint32_t lcap;
-    const uint32_t *lovf;     // the mask is read only when this is set
 };
 
 // gb_sieve_segment: the wheel-class window sieve of the verify kernel (shared memory,
@@ -212,10 +184,6 @@ struct gb_ctx {
     uint4 *pk;             // (p, kTileM mod p, rA, rB)
     uint32_t *carry;       // verify-kernel carried offsets: carry_ctas x carry_stride
     uint32_t *lmask;       // K-LARGE chunk mask (null when hi_max needs no primes > kCarryPrimeMax)
-    uint32_t *lbkt, *lfill, *lovf;  // K-LARGE per-tile hit lists (with lmask)
-    uint32_t lcap;
-    uint32_t *lbatch;      // K-LARGE hit-balanced prime batches
-    uint32_t n_lbatch;
     uint64_t lmask_stride; // u32 words per class
     uint64_t carry_stride;
     uint32_t carry_ctas;

@@ -401,131 +401,6 @@ __global__ void __launch_bounds__(kLargeBlock) large_mark_wheel_kernel(LargeArgs
     }
 }
 
-// K-LARGE bucket mode (gb_verify_range): the same cofactor-wheel walk, but a hit is
-// not an L2 atomic: it becomes an entry (class << 31 | bit position in the tile's
-// window) of the list of every verify tile whose window holds it, which the verify
-// kernel applies with shared-memory REDs.  One CTA per SM walks a contiguous share of
-// the primes in batches; entries are staged per tile in shared memory and flushed
-// after each batch with one global reservation per (batch, tile).  A staging slot or
-// a list that is full sends the hit to the L2 mask instead and raises *ovf (the verify
-// kernel then also ANDs the mask).
-__device__ __forceinline__ void bucket_spill(const LargeArgs &a, uint32_t cls, uint32_t m, uint64_t pol)
-{
-    uint32_t *w = (cls ? a.mask + a.stride : a.mask) + (m >> 5);
-    gmem_and(w, clear_mask(m), pol);
-    if (*(volatile uint32_t *)a.ovf == 0) atomicExch(a.ovf, 1u);
-}
-
-__global__ void __launch_bounds__(kBucketThreads) large_bucket_kernel(LargeArgs a, uint32_t tw_magic)
-{
-    extern __shared__ uint32_t bsm[];
-    uint32_t *stage = bsm;                                  // nt x kBucketStage
-    uint32_t *cnt = bsm + a.nt * kBucketStage;             // nt
-    uint32_t *base = cnt + a.nt;                            // nt
-    __shared__ uint8_t s_next[210];
-    __shared__ uint8_t s_res[48], s_gap[48];
-    const int tid = threadIdx.x;
-    for (int i = tid; i < 48; i += blockDim.x) {
-        s_res[i] = c_w210.res[i];
-        s_gap[i] = c_w210.gap[i];
-    }
-    for (int r = tid; r < 210; r += blockDim.x) {
-        int j = 0;
-        while (c_w210.res[j] < r) ++j;
-        s_next[r] = (uint8_t)j;
-    }
-    for (uint32_t t = tid; t < a.nt; t += blockDim.x) cnt[t] = 0;
-    __syncthreads();
-    const int64_t m_lo = a.g0 * 32;
-    const uint32_t nbits = 32 * a.nw;
-    const uint64_t q_base = 6 * (uint64_t)m_lo;
-    const uint64_t lim_off = 6ull * nbits;
-    const uint64_t q_first = m_lo > 0 ? q_base : 0;
-    const uint64_t pol = l2_keep_policy();
-    // this CTA's batches: blockIdx.x, blockIdx.x + gridDim.x, ... (hit-balanced)
-    // one entry for tile t (window word x - t tw)
-    auto put = [&](uint32_t t, uint32_t cls, uint32_t x, uint32_t bit, uint32_t m) {
-        const uint32_t slot = atomicAdd(cnt + t, 1u);
-        if (slot < (uint32_t)kBucketStage) stage[t * kBucketStage + slot] = (cls << 31) | (((x - t * a.tw) << 5) | bit);
-        else bucket_spill(a, cls, m, pol);
-    };
-    for (uint32_t bi = blockIdx.x; bi < a.n_batch; bi += gridDim.x) {
-        const uint64_t b0 = max((uint64_t)__ldg(a.batch + bi), (uint64_t)a.i_begin);
-        const uint64_t b1 = min((uint64_t)__ldg(a.batch + bi + 1), (uint64_t)a.i_end);
-        for (uint64_t pi = b0 + tid; pi < b1; pi += blockDim.x) {
-            const uint64_t p = __ldcs(a.primes + pi);
-            uint64_t k = p;
-            if (q_first > p * p) {
-                const uint64_t x = q_first + p - 1;
-                uint64_t quo = __umul64hi(x, __ldcs(a.magic + pi));
-                uint64_t rem = x - quo * p;
-                while (rem >= p) { ++quo; rem -= p; }
-                k = quo;
-            }
-            constexpr uint32_t kM = 210u * 11 * 13 * 17 * 19;
-            const uint32_t km = (uint32_t)(k % kM);
-            const uint32_t kr = km % 210;
-            const uint32_t idx0 = s_next[kr];
-            const uint32_t adv = s_res[idx0] - kr;
-            k += adv;
-            uint32_t idx = idx0;
-            uint64_t off = p * k - q_base;
-            if (off >= lim_off) continue;
-            const uint32_t kk = km + adv;
-            uint32_t r11 = kk % 11, r13 = kk % 13, r17 = kk % 17, r19 = kk % 19;
-            while (off < lim_off) {
-                const uint32_t o = (uint32_t)off;
-                const uint32_t m = __umulhi(o, 0xAAAAAAABu) >> 2;     // o / 6
-                if (r11 && r13 && r17 && r19) {
-                    const uint32_t cls = o - 6 * m == 1 ? 0u : 1u;
-                    const uint32_t x = m >> 5, bit = m & 31;
-                    uint32_t t = __umulhi(x, tw_magic);                // x / tw, maybe 1 low
-                    if ((t + 1) * a.tw <= x) ++t;
-                    if (t < a.nt) put(t, cls, x, bit, m);
-                    if (t >= 1 && t - 1 < a.nt && x - (t - 1) * a.tw < a.span) put(t - 1, cls, x, bit, m);
-                }
-                const uint32_t g = s_gap[idx];
-                idx = idx == 47 ? 0 : idx + 1;
-                off += p * g;
-                r11 += g; if (r11 >= 11) r11 -= 11;
-                r13 += g; if (r13 >= 13) r13 -= 13;
-                r17 += g; if (r17 >= 17) r17 -= 17;
-                r19 += g; if (r19 >= 19) r19 -= 19;
-            }
-        }
-        __syncthreads();
-        // flush: one global reservation per (batch, tile), all issued at once; then one
-        // warp per tile copies its staged entries into the list
-        for (uint32_t t = tid; t < a.nt; t += blockDim.x) {
-            const uint32_t c = min(cnt[t], (uint32_t)kBucketStage);
-            cnt[t] = c;
-            base[t] = c ? atomicAdd(a.fill + t, c) : 0u;
-        }
-        __syncthreads();
-        for (uint32_t t = tid >> 5; t < a.nt; t += blockDim.x >> 5) {
-            const uint32_t c = cnt[t], b0t = base[t];
-            for (uint32_t i = tid & 31; i < c; i += 32) {
-                const uint32_t e = stage[t * kBucketStage + i];
-                if (b0t + i < a.cap) {
-                    a.bkt[(uint64_t)t * a.cap + b0t + i] = e;
-                } else {                                          // list full: the mask takes it
-                    const uint32_t b = e & 0x7FFFFFFFu;
-                    bucket_spill(a, e >> 31, t * a.tw * 32 + b, pol);
-                }
-            }
-        }
-        __syncthreads();
-        for (uint32_t t = tid; t < a.nt; t += blockDim.x) cnt[t] = 0;
-        __syncthreads();
-    }
-}
-
-__global__ void large_bucket_reset_kernel(uint32_t *fill, uint32_t nt, uint32_t *ovf)
-{
-    for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) fill[i] = 0;
-    if (threadIdx.x == 0) *ovf = 0;
-}
-
 // ---------------------------------------------------------------------------
 // result vector
 // ---------------------------------------------------------------------------
@@ -603,20 +478,6 @@ cudaError_t launch_large(const LargeArgs &a, int num_sms, cudaStream_t st)
     const uint64_t n = a.i_end - a.i_begin;
     // large_mark_wheel_kernel keeps integer offsets 6 * 32 * nw in 32 bits
     if ((uint64_t)a.nw * 192 >= (1ull << 32)) return cudaErrorInvalidValue;
-    if (a.bkt) {
-        large_bucket_reset_kernel<<<1, 1024, 0, st>>>(a.fill, a.nt, a.ovf);
-        count_launch();
-        static std::atomic<uint64_t> done{0};
-        const int smem = (int)(4 * (uint64_t)a.nt * (kBucketStage + 2));
-        constexpr int kBucketSmemMax = 200 * 1024 / kBucketCtasPerSm;   // + static tables, per CTA
-        const cudaError_t attr = ensure_dyn_smem((const void *)large_bucket_kernel, kBucketSmemMax, done);
-        if (attr != cudaSuccess) return attr;
-        if (smem > kBucketSmemMax || a.span >= 2 * a.tw) return cudaErrorInvalidValue;
-        const uint32_t tw_magic = (uint32_t)((1ull << 32) / a.tw);
-        large_bucket_kernel<<<(unsigned)(kBucketCtasPerSm * num_sms), kBucketThreads, smem, st>>>(a, tw_magic);
-        count_launch();
-        return cudaGetLastError();
-    }
     const uint64_t nb = std::min<uint64_t>((n + kLargeBlock - 1) / kLargeBlock, (uint64_t)kLargeGridPerSm * num_sms);
     large_mark_wheel_kernel<<<(unsigned)nb, kLargeBlock, 0, st>>>(a);
     count_launch();

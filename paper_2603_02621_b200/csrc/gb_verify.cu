@@ -48,11 +48,6 @@ __host__ __device__ constexpr Trans trans(int a, uint32_t p)
 }
 
 constexpr int kK = 192;          // unrolled candidates per class
-#ifdef GB_AB_H64
-constexpr int kHcOff = 2;        // histc row: A_J at [J + kHcOff]
-#else
-constexpr int kHcOff = 1;
-#endif
 constexpr int kP1 = 56;          // phase 1: candidates every word goes through
 constexpr uint32_t kWinSlack = kWinSlackWords;   // words past a window phase-1 lanes may read (U = 0)
 constexpr int kQueue = kQueueEntries;   // per-warp survivor queue (<= 31 carried + 32 kW per round)
@@ -228,8 +223,7 @@ __device__ __forceinline__ void carry_st(uint32_t *p, uint32_t v, uint64_t pol)
 template <bool DEF_TILE>
 __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
                               Carry6 *cy, const MedSched &ms, uint32_t i_b2, uint32_t i_b1,
-                              const uint32_t *__restrict__ lm, int64_t lg0, uint64_t lstride,
-                              const uint32_t *__restrict__ bk, uint32_t bn, int tid)
+                              const uint32_t *__restrict__ lm, int64_t lg0, uint64_t lstride, int tid)
 {
     const uint32_t lane = (uint32_t)tid & 31;
     constexpr int nt = kThreads;
@@ -342,19 +336,6 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
         sh_hB[pi - sp.i_med] = (uint16_t)(ob < nbits ? (nbits - ob + k.x - 1) / k.x : 0);
     }
     __syncthreads();
-    // K-LARGE hit list of this tile (primes above the carried range): window bit
-    // positions, class in bit 31
-    for (uint32_t i0 = tid; i0 < bn; i0 += 4 * nt) {     // 4 loads in flight per thread
-        uint32_t e[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) e[k] = i0 + k * nt < bn ? __ldcs(bk + i0 + k * nt) : 0xFFFFFFFFu;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (e[k] != 0xFFFFFFFFu) {
-                const uint32_t b = e[k] & 0x7FFFFFFFu;
-                smem_and(((e[k] >> 31) ? sB : sA) + ((b >> 5) << 2), clear_mask(b));
-            }
-    }
     // one warp per medium prime: the host's LPT schedule (longest work first onto
     // the least-loaded warp) gives every sieving warp the same share, no atomics
     {
@@ -574,18 +555,9 @@ __device__ __forceinline__ void hist8(uint32_t c0, uint32_t c1, uint32_t c2, uin
     const uint32_t t1 = __reduce_add_sync(FULL, c2 + (c3 << 16));
     const uint32_t t2 = __reduce_add_sync(FULL, c4 + (c5 << 16));
     const uint32_t t3 = __reduce_add_sync(FULL, c6 + (c7 << 16));
-#ifdef GB_AB_H64
-    // lanes 0..3 add the pair (J + 2 lane, J + 2 lane + 1) as one 64-bit shared atomic
-    // (32-bit halves: a tile's count per candidate stays far below 2^32)
-    const uint32_t ts = (lane & 2) ? ((lane & 1) ? t3 : t2) : ((lane & 1) ? t1 : t0);
-    if (lane < 4)
-        atomicAdd((unsigned long long *)h + lane,
-                  (unsigned long long)(ts & 0xffffu) | ((unsigned long long)(ts >> 16) << 32));
-#else
     const uint32_t ts = (lane & 4) ? ((lane & 2) ? t3 : t2) : ((lane & 2) ? t1 : t0);
     const uint32_t v = (lane & 1) ? (ts >> 16) : (ts & 0xffffu);
     if (lane < 8 && v) atomicAdd(h + lane, v);
-#endif
 }
 
 template <int A, int J, bool DUMP>
@@ -1012,12 +984,7 @@ extern __shared__ uint32_t g_win[];
 
 struct Shared6 {
     uint32_t hist[kHistSmem];          // bins by prime index (runtime loop, fallback, specials)
-#ifdef GB_AB_H64
-    alignas(8) uint32_t histc[3][kK + 2];   // per class: [0] evens entering the table, [J + 2] = A_J (hist8,
-                                            // 64-bit pairs (J, J+1) at 8-byte aligned [J + 2])
-#else
     uint32_t histc[3][kK + 1];         // per class: [0] evens entering the table, [J + 1] = A_J (hist8)
-#endif
     uint32_t next_round[2];            // per window slot
     uint32_t ns[2];
     uint32_t q_base;      // word offset of the queues in dynamic shared memory
@@ -1056,7 +1023,7 @@ struct ClassWork {
         m.U = U;
         m.lb = 0; m.lu = 0;
         m.dump_w = DUMP ? a.dump + ((int64_t)(192 * u + A) - (int64_t)a.lo_e) / 2 : nullptr;
-        phase2<A, kP1, DUMP>(m, sh.histc[A / 2] + kHcOff, lane);
+        phase2<A, kP1, DUMP>(m, sh.histc[A / 2] + 1, lane);
         replay_key<A>(m, u, a, best_p, acc);
         constexpr uint32_t j_next = kTab[A / 2].bin[kK - 1] - 1;   // odd-list index after the table
         finish_word<A, DUMP>(m.U, j_next, m.wa, m.wb, u, sh.hist, a, acc, lane);
@@ -1108,7 +1075,7 @@ struct ClassWork {
                 atomicAdd(&acc->evens, (unsigned long long)(c >> 16));
             }
         }
-        phase1q<A, 0, kC1, DUMP, TRACK>(m, sh.histc[A / 2] + kHcOff, lane);
+        phase1q<A, 0, kC1, DUMP, TRACK>(m, sh.histc[A / 2] + 1, lane);
         if (TRACK) replay_key_q<A>(m, u0 + li0, a, best_p, acc);
         // survivors of candidates [0, kC1): staged past the queue's live entries,
         // then compacted to 2 (or 1) words per lane for candidates [kC1, kP1)
@@ -1158,7 +1125,7 @@ struct ClassWork {
             if (DUMP) m.dump[k] = a.dump + ((int64_t)(192 * (u0 + li) + A) - (int64_t)a.lo_e) / 2;
         }
         __syncwarp();                          // staged entries read before any append
-        phase1r<A, kC1, S, DUMP, TRACK>(m, sh.histc[A / 2] + kHcOff, lane);
+        phase1r<A, kC1, S, DUMP, TRACK>(m, sh.histc[A / 2] + 1, lane);
         if (TRACK) replay_key_r<A, S>(m, u0, a, best_p, acc);
 #pragma unroll
         for (int k = 0; k < S; ++k) {
@@ -1255,13 +1222,12 @@ __device__ __forceinline__ void flush_hist(Shared6 &sh, const VerifyArgs &a, Cta
             sh.hist[i] = 0;
         }
     }
-    static_assert(3 * (kK + kHcOff) <= kThreads, "one class-table entry per thread");
+    static_assert(3 * (kK + 1) <= kThreads, "one class-table entry per thread");
     uint32_t v = 0;
     const int c = tid / kK, j = tid % kK;
-    if (tid < 3 * kK)                                                  // A_{j-1} - A_j
-        v = sh.histc[c][j == 0 ? 0 : j - 1 + kHcOff] - sh.histc[c][j + kHcOff];
+    if (tid < 3 * kK) v = sh.histc[c][j] - sh.histc[c][j + 1];      // A_{j-1} - A_j
     __syncthreads();
-    if (tid < 3 * (kK + kHcOff)) (&sh.histc[0][0])[tid] = 0;
+    if (tid < 3 * (kK + 1)) (&sh.histc[0][0])[tid] = 0;
     uint64_t sp = 0;
     if (v) {
         sp = (uint64_t)v * c_tab[c].p[j];
@@ -1287,7 +1253,7 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant_
     const uint32_t nw_max = halo + a.tile_words + kWinSlack;
     if (tid == 0) sh.q_base = 2 * nw_max;
     for (int i = tid; i < kHistSmem; i += kThreads) sh.hist[i] = 0;
-    for (int i = tid; i < 3 * (kK + kHcOff); i += kThreads) (&sh.histc[0][0])[i] = 0;
+    for (int i = tid; i < 3 * (kK + 1); i += kThreads) (&sh.histc[0][0])[i] = 0;
     if (tid == 0) sh.acc = CtaAcc{0, 0, 0, 0, 0, ~0ull, 0};
     CtaAcc *const acc = &sh.acc;
     uint32_t best_p = 0;                       // per warp: replay only blocks that can raise the max
@@ -1305,10 +1271,6 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant_
         const int64_t g0 = (int64_t)u0 - (int64_t)halo;
         uint32_t *wA = win, *wB = win + nw_max;
         __syncthreads();                      // previous tile fully consumed
-        const uint64_t tile = t_begin + t;
-        const uint32_t *bk = a.lbkt ? a.lbkt + tile * a.lcap : nullptr;
-        const uint32_t bn = a.lbkt ? min(__ldg(a.lfill + tile), a.lcap) : 0u;
-        const uint32_t *lm = (a.lbkt == nullptr || *a.lovf) ? a.lmask : nullptr;
         {
             Carry6 cy;
             cy.off = a.carry + (uint64_t)blockIdx.x * 2 * a.carry_stride;
@@ -1327,11 +1289,11 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant_
             cy.init = sh.ns[0] >> 31;
             const MedSched med{a.med_idx, a.med_off};
             if (cy.tile_m == kTileM)
-                sieve6_window<true>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, lm, a.lmask_g0,
-                                    a.lmask_stride, bk, bn, tid);
+                sieve6_window<true>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask, a.lmask_g0,
+                                    a.lmask_stride, tid);
             else
-                sieve6_window<false>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, lm, a.lmask_g0,
-                                     a.lmask_stride, bk, bn, tid);
+                sieve6_window<false>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask, a.lmask_g0,
+                                     a.lmask_stride, tid);
         }
         __syncthreads();
         mark_tile<DUMP, UNROLL>(sh, sh.next_round[0], u0, tw, wA, wB, halo, a, acc, best_p, lane, warp);
@@ -1397,10 +1359,10 @@ __global__ void __launch_bounds__(kThreads) sieve_out_kernel(const __grid_consta
         cy.init = sh_ns >> 31;
         if (cy.tile_m == kTileM)
             sieve6_window<true>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
-                                a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride, nullptr, 0u, tid);
+                                a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride, tid);
         else
             sieve6_window<false>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
-                                 a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride, nullptr, 0u, tid);
+                                 a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride, tid);
         cy.have_prev = true;
         __syncthreads();
         for (uint32_t i = tid; i < tw; i += kThreads) {
