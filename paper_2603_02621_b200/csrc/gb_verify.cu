@@ -1007,7 +1007,11 @@ struct ClassWork {
     // (everything by value: no local-memory round trip of the caller's state; the
     // queue entries [qn - take, qn) are consumed, the caller lowers qn; returns the
     // updated running max best_p)
+#ifdef GB_AB_INLINEB
+    static __device__ __forceinline__ uint32_t batch(Shared6 &sh, uint32_t qn, uint32_t take, uint64_t u0,
+#else
     static __device__ __noinline__ uint32_t batch(Shared6 &sh, uint32_t qn, uint32_t take, uint64_t u0,
+#endif
                                                   const uint32_t *wA, const uint32_t *wB, uint32_t halo,
                                                   const VerifyArgs &a, CtaAcc *acc, uint32_t best_p, int lane,
                                                   int warp)
@@ -1097,10 +1101,12 @@ struct ClassWork {
             if (cnt > 32) stage<2, TRACK>(sh, qn, q0 + base, cnt, u0, wA, wB, halo, a, acc, best_p, lane, warp);
             else stage<1, TRACK>(sh, qn, q0 + base, cnt, u0, wA, wB, halo, a, acc, best_p, lane, warp);
         }
+#ifndef GB_AB_INLINEB
         while (qn >= 32) {
             best_p = batch(sh, qn, 32, u0, wA, wB, halo, a, acc, best_p, lane, warp);
             qn -= 32;
         }
+#endif
     }
 
     // candidates [kC1, kP1) for cnt staged words at queue entries e0.. (S per lane);
@@ -1191,6 +1197,33 @@ __device__ __forceinline__ void mark_tile(Shared6 &sh, uint32_t &next_round, uin
     const uint32_t r1 = (tw + 32 * kW - 1) / (32 * kW);
     uint32_t qn = 0;
     int qcls = 0;
+#ifdef GB_AB_INLINEB
+    // phase-2 batches run here, between rounds, from one inlined copy per class: no
+    // out-of-line call (whose ABI would save the caller's live registers to local
+    // memory); the queue is drained below 32 before every round (a round adds <= 96
+    // of the 128 entries) and emptied at a class change and at the end
+    while (true) {
+        uint32_t r = 0;
+        if (lane == 0) r = atomicAdd(&next_round, 1u);
+        r = __shfl_sync(FULL, r, 0);
+        const bool last = r >= 3 * r1;
+        const int cls = last ? -1 : (r >= r1 ? (r >= 2 * r1 ? 2 : 1) : 0);
+        const uint32_t keep = cls == qcls ? 31u : 0u;
+        while (UNROLL && qn > keep) {
+            const uint32_t take = min(qn, 32u);
+            if (qcls == 0) best_p = ClassWork<0, DUMP, UNROLL>::batch(sh, qn, take, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+            else if (qcls == 1) best_p = ClassWork<2, DUMP, UNROLL>::batch(sh, qn, take, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+            else best_p = ClassWork<4, DUMP, UNROLL>::batch(sh, qn, take, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+            qn -= take;
+        }
+        if (last) break;
+        qcls = cls;
+        const uint32_t pair = r - (uint32_t)cls * r1;
+        if (cls == 0) ClassWork<0, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+        else if (cls == 1) ClassWork<2, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+        else ClassWork<4, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+    }
+#else
     while (true) {
         uint32_t r = 0;
         if (lane == 0) r = atomicAdd(&next_round, 1u);
@@ -1207,6 +1240,7 @@ __device__ __forceinline__ void mark_tile(Shared6 &sh, uint32_t &next_round, uin
         else ClassWork<4, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
     }
     flush_queue<DUMP, UNROLL>(qcls, sh, qn, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+#endif
 }
 
 // shared histograms -> result vector (all threads; callers barrier around it).  The
