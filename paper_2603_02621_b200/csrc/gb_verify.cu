@@ -1000,18 +1000,14 @@ __device__ __forceinline__ uint16_t *sh_qli(const Shared6 &sh, int warp)
     return (uint16_t *)(g_win + sh.q_base + kMarkWarps * kQueue) + (uint32_t)warp * kQueue;
 }
 
-template <int A, bool DUMP, bool UNROLL>
+template <int A, bool DUMP, bool UNROLL, bool INB>
 struct ClassWork {
     // one phase-2 batch of `take` queued words of class A (out of line: called from
     // the round loop and the queue flushes; keeps the hot code small)
     // (everything by value: no local-memory round trip of the caller's state; the
     // queue entries [qn - take, qn) are consumed, the caller lowers qn; returns the
     // updated running max best_p)
-#ifdef GB_AB_INLINEB
-    static __device__ __forceinline__ uint32_t batch(Shared6 &sh, uint32_t qn, uint32_t take, uint64_t u0,
-#else
-    static __device__ __noinline__ uint32_t batch(Shared6 &sh, uint32_t qn, uint32_t take, uint64_t u0,
-#endif
+    static __device__ __forceinline__ uint32_t batch_body(Shared6 &sh, uint32_t qn, uint32_t take, uint64_t u0,
                                                   const uint32_t *wA, const uint32_t *wB, uint32_t halo,
                                                   const VerifyArgs &a, CtaAcc *acc, uint32_t best_p, int lane,
                                                   int warp)
@@ -1032,6 +1028,24 @@ struct ClassWork {
         constexpr uint32_t j_next = kTab[A / 2].bin[kK - 1] - 1;   // odd-list index after the table
         finish_word<A, DUMP>(m.U, j_next, m.wa, m.wb, u, sh.hist, a, acc, lane);
         return best_p;
+    }
+    static __device__ __noinline__ uint32_t batch_call(Shared6 &sh, uint32_t qn, uint32_t take, uint64_t u0,
+                                                       const uint32_t *wA, const uint32_t *wB, uint32_t halo,
+                                                       const VerifyArgs &a, CtaAcc *acc, uint32_t best_p, int lane,
+                                                       int warp)
+    {
+        return batch_body(sh, qn, take, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+    }
+    // INB: inlined at its single call site in mark_tile (the K-LARGE regime, where
+    // phase 2 runs often: 93.5 vs 95.9 ms on the C5 span); else out of line (the
+    // smaller hot loop wins at 1e12: 29.50 vs 29.69 ms)
+    static __device__ __forceinline__ uint32_t batch(Shared6 &sh, uint32_t qn, uint32_t take, uint64_t u0,
+                                                     const uint32_t *wA, const uint32_t *wB, uint32_t halo,
+                                                     const VerifyArgs &a, CtaAcc *acc, uint32_t best_p, int lane,
+                                                     int warp)
+    {
+        if constexpr (INB) return batch_body(sh, qn, take, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+        else return batch_call(sh, qn, take, u0, wA, wB, halo, a, acc, best_p, lane, warp);
     }
 
     // one phase-1 round: words pair*32kW + 32k + lane (k < kW) of class A
@@ -1101,12 +1115,12 @@ struct ClassWork {
             if (cnt > 32) stage<2, TRACK>(sh, qn, q0 + base, cnt, u0, wA, wB, halo, a, acc, best_p, lane, warp);
             else stage<1, TRACK>(sh, qn, q0 + base, cnt, u0, wA, wB, halo, a, acc, best_p, lane, warp);
         }
-#ifndef GB_AB_INLINEB
-        while (qn >= 32) {
-            best_p = batch(sh, qn, 32, u0, wA, wB, halo, a, acc, best_p, lane, warp);
-            qn -= 32;
+        if constexpr (!INB) {
+            while (qn >= 32) {
+                best_p = batch(sh, qn, 32, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+                qn -= 32;
+            }
         }
-#endif
     }
 
     // candidates [kC1, kP1) for cnt staged words at queue entries e0.. (S per lane);
@@ -1180,16 +1194,16 @@ __device__ __forceinline__ void flush_queue(int cls, Shared6 &sh, uint32_t &qn, 
                                             uint32_t &best_p, int lane, int warp)
 {
     if (!UNROLL || qn == 0) return;
-    if (cls == 0) best_p = ClassWork<0, DUMP, UNROLL>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
-    else if (cls == 1) best_p = ClassWork<2, DUMP, UNROLL>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
-    else best_p = ClassWork<4, DUMP, UNROLL>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+    if (cls == 0) best_p = ClassWork<0, DUMP, UNROLL, false>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+    else if (cls == 1) best_p = ClassWork<2, DUMP, UNROLL, false>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
+    else best_p = ClassWork<4, DUMP, UNROLL, false>::batch(sh, qn, qn, u0, wA, wB, halo, a, acc, best_p, lane, warp);
     qn = 0;
 }
 
 // marking of one tile: rounds of 32 kW words of one class, handed out dynamically
 // (class-major) through the shared counter `next_round`; qwarp indexes the
 // survivor queue of this warp
-template <bool DUMP, bool UNROLL>
+template <bool DUMP, bool UNROLL, bool INB>
 __device__ __forceinline__ void mark_tile(Shared6 &sh, uint32_t &next_round, uint64_t u0, uint32_t tw,
                                           const uint32_t *wA, const uint32_t *wB, uint32_t halo,
                                           const VerifyArgs &a, CtaAcc *acc, uint32_t &best_p, int lane, int qwarp)
@@ -1197,7 +1211,7 @@ __device__ __forceinline__ void mark_tile(Shared6 &sh, uint32_t &next_round, uin
     const uint32_t r1 = (tw + 32 * kW - 1) / (32 * kW);
     uint32_t qn = 0;
     int qcls = 0;
-#ifdef GB_AB_INLINEB
+    if constexpr (INB) {
     // phase-2 batches run here, between rounds, from one inlined copy per class: no
     // out-of-line call (whose ABI would save the caller's live registers to local
     // memory); the queue is drained below 32 before every round (a round adds <= 96
@@ -1211,19 +1225,19 @@ __device__ __forceinline__ void mark_tile(Shared6 &sh, uint32_t &next_round, uin
         const uint32_t keep = cls == qcls ? 31u : 0u;
         while (UNROLL && qn > keep) {
             const uint32_t take = min(qn, 32u);
-            if (qcls == 0) best_p = ClassWork<0, DUMP, UNROLL>::batch(sh, qn, take, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
-            else if (qcls == 1) best_p = ClassWork<2, DUMP, UNROLL>::batch(sh, qn, take, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
-            else best_p = ClassWork<4, DUMP, UNROLL>::batch(sh, qn, take, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+            if (qcls == 0) best_p = ClassWork<0, DUMP, UNROLL, true>::batch(sh, qn, take, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+            else if (qcls == 1) best_p = ClassWork<2, DUMP, UNROLL, true>::batch(sh, qn, take, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+            else best_p = ClassWork<4, DUMP, UNROLL, true>::batch(sh, qn, take, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
             qn -= take;
         }
         if (last) break;
         qcls = cls;
         const uint32_t pair = r - (uint32_t)cls * r1;
-        if (cls == 0) ClassWork<0, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
-        else if (cls == 1) ClassWork<2, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
-        else ClassWork<4, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+        if (cls == 0) ClassWork<0, DUMP, UNROLL, true>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+        else if (cls == 1) ClassWork<2, DUMP, UNROLL, true>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+        else ClassWork<4, DUMP, UNROLL, true>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
     }
-#else
+    } else {
     while (true) {
         uint32_t r = 0;
         if (lane == 0) r = atomicAdd(&next_round, 1u);
@@ -1235,12 +1249,12 @@ __device__ __forceinline__ void mark_tile(Shared6 &sh, uint32_t &next_round, uin
             flush_queue<DUMP, UNROLL>(qcls, sh, qn, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
             qcls = cls;
         }
-        if (cls == 0) ClassWork<0, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
-        else if (cls == 1) ClassWork<2, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
-        else ClassWork<4, DUMP, UNROLL>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+        if (cls == 0) ClassWork<0, DUMP, UNROLL, false>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+        else if (cls == 1) ClassWork<2, DUMP, UNROLL, false>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
+        else ClassWork<4, DUMP, UNROLL, false>::round(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
     }
     flush_queue<DUMP, UNROLL>(qcls, sh, qn, u0, wA, wB, halo, a, acc, best_p, lane, qwarp);
-#endif
+    }
 }
 
 // shared histograms -> result vector (all threads; callers barrier around it).  The
@@ -1277,7 +1291,8 @@ __device__ __forceinline__ void flush_hist(Shared6 &sh, const VerifyArgs &a, Cta
 // __grid_constant__: the cold out-of-line paths take `a` by reference; without it
 // the whole parameter block is copied to the local-memory stack and every field
 // read becomes a local load (long-scoreboard stalls in the hot loop).
-template <bool DUMP, bool UNROLL>
+// INB: phase-2 batches inlined (the K-LARGE regime, see ClassWork::batch).
+template <bool DUMP, bool UNROLL, bool INB>
 __global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant__ VerifyArgs a)
 {
     uint32_t *win = g_win;                     // slot windows (class A | class B) | queues
@@ -1330,7 +1345,7 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant_
                                      a.lmask_stride, tid);
         }
         __syncthreads();
-        mark_tile<DUMP, UNROLL>(sh, sh.next_round[0], u0, tw, wA, wB, halo, a, acc, best_p, lane, warp);
+        mark_tile<DUMP, UNROLL, INB>(sh, sh.next_round[0], u0, tw, wA, wB, halo, a, acc, best_p, lane, warp);
         // per-tile flush of the shared histograms keeps their 32-bit bins exact
         __syncthreads();
         flush_hist(sh, a, acc, tid);
@@ -1426,12 +1441,14 @@ __global__ void __launch_bounds__(kThreads) sieve_out_kernel(const __grid_consta
 // are ever launched with (kVerifySmemMax / kSieveOutSmemMax, gb_internal.h).
 cudaError_t configure_verify()
 {
-    static std::atomic<uint64_t> d0{0}, d1{0}, d2{0}, d3{0};
+    static std::atomic<uint64_t> d0{0}, d1{0}, d2{0}, d3{0}, d4{0}, d5{0};
     constexpr int sm = (int)kVerifySmemMax;
-    cudaError_t e = ensure_dyn_smem((const void *)verify_kernel<false, false>, sm, d0);
-    if (e == cudaSuccess) e = ensure_dyn_smem((const void *)verify_kernel<true, false>, sm, d1);
-    if (e == cudaSuccess) e = ensure_dyn_smem((const void *)verify_kernel<false, true>, sm, d2);
-    if (e == cudaSuccess) e = ensure_dyn_smem((const void *)verify_kernel<true, true>, sm, d3);
+    cudaError_t e = ensure_dyn_smem((const void *)verify_kernel<false, false, false>, sm, d0);
+    if (e == cudaSuccess) e = ensure_dyn_smem((const void *)verify_kernel<true, false, false>, sm, d1);
+    if (e == cudaSuccess) e = ensure_dyn_smem((const void *)verify_kernel<false, true, false>, sm, d2);
+    if (e == cudaSuccess) e = ensure_dyn_smem((const void *)verify_kernel<true, true, false>, sm, d3);
+    if (e == cudaSuccess) e = ensure_dyn_smem((const void *)verify_kernel<false, true, true>, sm, d4);
+    if (e == cudaSuccess) e = ensure_dyn_smem((const void *)verify_kernel<true, true, true>, sm, d5);
     return e;
 }
 
@@ -1450,7 +1467,7 @@ int verify_blocks_per_sm(size_t smem)
 {
     int nb = 0;
     if (configure_verify() != cudaSuccess) return 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, verify_kernel<false, true>, kThreads, smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, verify_kernel<false, true, false>, kThreads, smem) !=
         cudaSuccess)
         return 1;
     return nb < 1 ? 1 : nb;
@@ -1462,12 +1479,15 @@ cudaError_t launch_verify(const VerifyArgs &a, int grid, size_t smem, cudaStream
     const cudaError_t e = configure_verify();
     if (e != cudaSuccess) return e;
     const bool unroll = a.p_fallback - 2 >= kUnrollPMax;   // p_fallback = largest candidate + 2
+    const bool inb = a.lmask != nullptr;                    // K-LARGE regime (hi > 2^42): inlined batches
     if (a.dump) {
-        if (unroll) verify_kernel<true, true><<<grid, kThreads, smem, st>>>(a);
-        else verify_kernel<true, false><<<grid, kThreads, smem, st>>>(a);
+        if (unroll && inb) verify_kernel<true, true, true><<<grid, kThreads, smem, st>>>(a);
+        else if (unroll) verify_kernel<true, true, false><<<grid, kThreads, smem, st>>>(a);
+        else verify_kernel<true, false, false><<<grid, kThreads, smem, st>>>(a);
     } else {
-        if (unroll) verify_kernel<false, true><<<grid, kThreads, smem, st>>>(a);
-        else verify_kernel<false, false><<<grid, kThreads, smem, st>>>(a);
+        if (unroll && inb) verify_kernel<false, true, true><<<grid, kThreads, smem, st>>>(a);
+        else if (unroll) verify_kernel<false, true, false><<<grid, kThreads, smem, st>>>(a);
+        else verify_kernel<false, false, false><<<grid, kThreads, smem, st>>>(a);
     }
     count_launch();
     return cudaGetLastError();
