@@ -1270,18 +1270,26 @@ __device__ __forceinline__ void flush_hist(Shared6 &sh, const VerifyArgs &a, Cta
             sh.hist[i] = 0;
         }
     }
-    static_assert(3 * (kK + 1) <= kThreads, "one class-table entry per thread");
-    uint32_t v = 0;
-    const int c = tid / kK, j = tid % kK;
-    if (tid < 3 * kK) v = sh.histc[c][j] - sh.histc[c][j + 1];      // A_{j-1} - A_j
-    __syncthreads();
-    if (tid < 3 * (kK + 1)) (&sh.histc[0][0])[tid] = 0;
-    uint64_t sp = 0;
-    if (v) {
-        sp = (uint64_t)v * c_tab[c].p[j];
-        atomicAdd(R + GB_R_HIST + c_tab[c].bin[j], (unsigned long long)v);
+    constexpr int kHc = 3 * kK;                                        // class-table entries
+    constexpr int kPer = (kHc + kThreads - 1) / kThreads;              // per thread
+    uint32_t v[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const int i = tid + q * kThreads, c = i / kK, j = i % kK;
+        v[q] = i < kHc ? sh.histc[c][j] - sh.histc[c][j + 1] : 0u;      // A_{j-1} - A_j
     }
-    if (tid < 3 * kK) {                                   // warps 0..17: share of sum p_min
+    __syncthreads();
+    for (int i = tid; i < 3 * (kK + 1); i += kThreads) (&sh.histc[0][0])[i] = 0;
+    uint64_t sp = 0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const int i = tid + q * kThreads, c = i / kK, j = i % kK;
+        if (v[q]) {
+            sp += (uint64_t)v[q] * c_tab[c].p[j];
+            atomicAdd(R + GB_R_HIST + c_tab[c].bin[j], (unsigned long long)v[q]);
+        }
+    }
+    if (tid < kHc) {                                   // the warps holding entries: share of sum p_min
         for (int o = 16; o; o >>= 1) sp += __shfl_xor_sync(FULL, sp, o);
         if ((tid & 31) == 0 && sp) atomicAdd(&acc->sum, (unsigned long long)sp);
     }
