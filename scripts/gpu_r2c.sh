@@ -44,15 +44,33 @@ for w in $what; do
         python bench.py --workload c5 --steps 1 --warmup 1 --no-cpu-baseline --no-check > /dev/null 2>&1
       echo "ncu launches c5 rc=$?"
       F="$N --set full --import-source on -c 1 -f"
+      S="python scripts/ncu_summary.py"
+      # each capture is summarised here (ncu -i works on the box) and only the C4
+      # verify report is kept: gpurun copies back at most 64 MiB
       $F -k regex:verify_kernel -o gpurun_out/prof_verify_c4 python scripts/prof_one.py --span 36 > gpurun_out/prof_c4.log 2>&1
       echo "ncu verify c4 rc=$?"
+      $S gpurun_out/prof_verify_c4.ncu-rep gpurun_out/sum_verify_kernel_c4 --evens 34359738368 \
+        --note "ncu --set full --clock-control none, one gb_verify_range over the top 2^36 integers of [4, 1e12] (scripts/prof_one.py --span 36)" > /dev/null
       $F -k regex:sieve_out -o gpurun_out/prof_sieve_c4 python scripts/prof_one.py --span 34 > /dev/null 2>&1
       echo "ncu sieve c4 rc=$?"
+      $S gpurun_out/prof_sieve_c4.ncu-rep gpurun_out/sum_sieve_out_kernel_c4 --evens 8589934592 \
+        --note "ncu --set full, gb_sieve_segment (sieve_out_kernel) over the top 2^34 integers of [4, 1e12] (evens = integers / 2)" > /dev/null
+      rm -f gpurun_out/prof_sieve_c4.ncu-rep
       $F -k regex:verify_kernel -o gpurun_out/prof_verify_c5 python scripts/prof_one.py --hi 4000000000000000000 --span 34 > /dev/null 2>&1
       echo "ncu verify c5 rc=$?"
+      $S gpurun_out/prof_verify_c5.ncu-rep gpurun_out/sum_verify_kernel_c5 --evens 872939520 \
+        --note "ncu --set full, the first verify launch (one K-LARGE chunk: 444 tiles = 8.73e8 evens) of the top 2^34 integers of [4e18 - 1e11, 4e18)" > /dev/null
+      rm -f gpurun_out/prof_verify_c5.ncu-rep
       $F -k regex:large_mark -o gpurun_out/prof_large_c5 python scripts/prof_one.py --hi 4000000000000000000 --span 34 > /dev/null 2>&1
       echo "ncu large c5 rc=$?"
+      $S gpurun_out/prof_large_c5.ncu-rep gpurun_out/sum_large_mark_wheel_kernel_c5 --evens 872939520 \
+        --note "ncu --set full, the first K-LARGE mark launch (one chunk: 444 tiles = 8.73e8 evens) of the top 2^34 integers of the C5 window" > /dev/null
+      rm -f gpurun_out/prof_large_c5.ncu-rep
       $F -k regex:counts_kernel -o gpurun_out/prof_counts python bench.py --mode counts --steps 1 --warmup 1 --no-check > /dev/null 2>&1
-      echo "ncu counts rc=$?" ;;
+      echo "ncu counts rc=$?"
+      $S gpurun_out/prof_counts.ncu-rep gpurun_out/sum_counts_kernel_counts --evens 16384 \
+        --note "ncu --set full, gb_partition_counts of the top 16384 even n below 1e9 (bench.py --mode counts)" > /dev/null
+      rm -f gpurun_out/prof_counts.ncu-rep
+      ls -la gpurun_out | tail -30 ;;
   esac
 done
