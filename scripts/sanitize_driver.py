@@ -18,7 +18,7 @@ from paper_2603_02621_b200.verifier import Verifier  # noqa: E402
 
 
 def check(got, want, what):
-    for k in oracle.FIELDS:
+    for k in oracle.AGG_FIELDS:
         assert got[k] == want[k], (what, k, got[k], want[k])
 
 
@@ -34,6 +34,10 @@ for lo, hi, p in ((4, 2 * 10**5 + 1, 65521), (4, 5 * 10**4, 5), (999000, 10**6 +
 w = v.sieve_segment(0, 64).cpu().numpy().view(np.uint64)
 ob = oracle.sieve_window(3, 3 + 128 * 64)
 assert np.array_equal(w, np.packbits(ob, bitorder="little").view(np.uint64))
+# NEXT-4 partition counts and NEXT-3 single_check
+c = v.partition_counts(4, 20001).cpu().numpy().astype(np.uint64)
+assert np.array_equal(c, oracle.partition_counts(4, 20001))
+assert v.single_check(98) == 19 and v.single_check(10**6) == 17
 v.close()
 # K-LARGE (sieving primes above 2^21): a window at 1e13
 v = Verifier(hi_max=10**13 + 1, p_max=65521, origin=10**13 - 2**21)
