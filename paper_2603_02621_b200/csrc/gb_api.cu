@@ -416,6 +416,16 @@ gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_m
     if (hi <= lo_e) return GB_OK;                            // empty range: no launch
     if (hi > ctx->hi_max) return GB_ERANGE;
     if (lo_e < ctx->origin || ((hi - ctx->origin) >> 1) >= (1ull << GB_KEY_SHIFT)) return GB_EINVAL;
+    // A range that straddles 2^42 = kCarryPrimeMax^2 only needs the K-LARGE chunks
+    // above it: below, every sieving prime is carried in shared memory, so that part
+    // runs as one unchunked launch (results add; the dump continues at its offset)
+    constexpr uint64_t kSplit = (uint64_t)kCarryPrimeMax * kCarryPrimeMax;
+    if (lo_e < kSplit && hi > kSplit) {
+        gb_status st = gb_verify_range_ex(ctx, lo_e, kSplit, p_max, fallback_p_cap, d_result, d_pmin_dump, stream);
+        if (st != GB_OK) return st;
+        return gb_verify_range_ex(ctx, kSplit, hi, p_max, fallback_p_cap, d_result,
+                                  d_pmin_dump ? d_pmin_dump + (kSplit - lo_e) / 2 : nullptr, stream);
+    }
     VerifyArgs a;
     // wheel classes n = 6m + c (c = 0, 2, 4): valid m in [ceil((lo_e-c)/6), ceil((hi-c)/6))
     uint64_t mlo_min = UINT64_MAX, mhi_max = 0;
