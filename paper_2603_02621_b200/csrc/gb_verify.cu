@@ -221,7 +221,7 @@ __device__ __forceinline__ void carry_st(uint32_t *p, uint32_t v, uint64_t pol)
 
 // K-SIEVE of one tile's two class windows by the whole CTA; ends WITHOUT a barrier
 template <bool DEF_TILE>
-__device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
+__device__ __forceinline__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
                               Carry6 *cy, const MedSched &ms, uint32_t i_b2, uint32_t i_b1,
                               const uint32_t *__restrict__ lm, int64_t lg0, uint64_t lstride, int tid)
 {
@@ -480,6 +480,26 @@ __device__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t n
             cy->off[cy->stride + pi] = next_off6(ob, k.x, tm, cy->tile_m);
         }
     }
+}
+
+// The sieve as its own function (own register allocation, called once per tile):
+// below 2^42 the marking code then compiles without the sieve's pressure (29.31 vs
+// 29.51 ms at 1e12); in the K-LARGE regime inlined (93.05 vs 93.76 ms at 4e18).
+template <bool DEF_TILE>
+__device__ __noinline__ void sieve6_window_call(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw,
+                                                const SievePrimes &sp, Carry6 *cy, const MedSched &ms,
+                                                uint32_t i_b2, uint32_t i_b1, const uint32_t *__restrict__ lm,
+                                                int64_t lg0, uint64_t lstride, int tid)
+{
+    sieve6_window<DEF_TILE>(wA, wB, g0, nw, sp, cy, ms, i_b2, i_b1, lm, lg0, lstride, tid);
+}
+template <bool DEF_TILE, bool OUTLINE>
+__device__ __forceinline__ void sieve6(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
+                                       Carry6 *cy, const MedSched &ms, uint32_t i_b2, uint32_t i_b1,
+                                       const uint32_t *__restrict__ lm, int64_t lg0, uint64_t lstride, int tid)
+{
+    if constexpr (OUTLINE) sieve6_window_call<DEF_TILE>(wA, wB, g0, nw, sp, cy, ms, i_b2, i_b1, lm, lg0, lstride, tid);
+    else sieve6_window<DEF_TILE>(wA, wB, g0, nw, sp, cy, ms, i_b2, i_b1, lm, lg0, lstride, tid);
 }
 
 // ---------------------------------------------------------------------------
@@ -1346,11 +1366,11 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant_
             cy.init = sh.ns[0] >> 31;
             const MedSched med{a.med_idx, a.med_off};
             if (cy.tile_m == kTileM)
-                sieve6_window<true>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask, a.lmask_g0,
-                                    a.lmask_stride, tid);
+                sieve6<true, !INB>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask, a.lmask_g0,
+                                   a.lmask_stride, tid);
             else
-                sieve6_window<false>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask, a.lmask_g0,
-                                     a.lmask_stride, tid);
+                sieve6<false, !INB>(wA, wB, g0, halo + tw, a.sp, &cy, med, a.i_b2, a.i_b1, a.lmask, a.lmask_g0,
+                                    a.lmask_stride, tid);
         }
         __syncthreads();
         mark_tile<DUMP, UNROLL, INB>(sh, sh.next_round[0], u0, tw, wA, wB, halo, a, acc, best_p, lane, warp);
