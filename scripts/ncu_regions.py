@@ -18,7 +18,7 @@ MARKS = [
     ("sieve:clear_bit", r"^__device__ __forceinline__ void clear_bit"),
     ("sieve:medium progression", r"^__device__ __forceinline__ void mark_progression2"),
     ("sieve:carry policy", r"^__device__ __forceinline__ uint64_t carry_policy"),
-    ("sieve:window (tiny patterns)", r"^__device__ void sieve6_window"),
+    ("sieve:window (tiny patterns)", r"^__device__ __forceinline__ void sieve6_window\("),
     ("sieve:medium setup", r"^\s*// medium primes \(31 < p"),
     ("sieve:medium warp loop", r"^\s*// one warp per medium prime"),
     ("sieve:steady large", r"^\s*// large primes: one thread per prime"),
