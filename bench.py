@@ -231,6 +231,30 @@ def load_peaks():
     return peaks, pint
 
 
+def launch_shares(wl: str):
+    """Per-kernel GPU-time shares from the newest committed ncu launch list of this
+    workload (profiles/r<NN>_launches_<wl>.md, scripts/launch_list.py), or None."""
+    import glob
+    lists = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_launches_{wl}.md")))
+    if not lists:
+        return None, None
+    ns = {}
+    for line in open(lists[-1]):
+        parts = [x.strip() for x in line.split("|")]
+        if len(parts) > 4 and parts[3].isdigit():
+            ns[parts[1]] = int(parts[3])
+    return ns, os.path.relpath(lists[-1], ROOT)
+
+
+# K-LARGE (gb_kernels.cu large_mark_wheel_kernel): a sieving prime p > 2^21 clears
+# q = p k only for cofactors k coprime to every prime <= 19 (the others are cleared by
+# the window's own sieve): density prod_{p <= 19} (1 - 1/p) of the integers k
+KLARGE_DENSITY = 1.0
+for _q in (2, 3, 5, 7, 11, 13, 17, 19):
+    KLARGE_DENSITY *= 1 - 1 / _q
+KLARGE_PRIME_MIN = 1 << 21          # kCarryPrimeMax (gb_internal.h)
+
+
 def ncu_capture(kernel: str, wl: str, mode: str):
     """The committed ncu --set full summary of `kernel` on this workload
     (profiles/r<NN>_<kernel>_<workload>[_<mode>].json, newest round first), or None."""
@@ -627,6 +651,38 @@ def main():
         roofline["mark"] = {"bound": "alu", "achieved": mark_ach, "peak": alu_peak, "unit": "Tops/s",
                             "frac": mark_ach / alu_peak, "est_share_of_kernel": t_mark / avg_launch_s,
                             "basis": "verify_kernel time minus the sieve share; 6 ops x SURVEY word-iterations"}
+
+    # ---- K-LARGE (ranges above 2^42): no-return L2 REDs into the chunk mask.  Its
+    # roofline is the L2 RED rate (profiles/r02b_red_sms.json, 64 MB L2-resident buffer,
+    # all SMs); its time is the step time x its share of the GPU time in the committed
+    # launch list of this workload (cold-cache / serialised: a share, not a time)
+    if args.mode == "bulk" and sqrt_hi > KLARGE_PRIME_MIN:
+        split = KLARGE_PRIME_MIN * KLARGE_PRIME_MIN
+        frac_above = (hi - max(lo, split)) / (hi - lo)
+        reds_per_even = 2 * KLARGE_DENSITY * recip_sum(KLARGE_PRIME_MIN, sqrt_hi)
+        ns, ls_src = launch_shares(wl_key)
+        red_peak_s = None
+        try:
+            rs = json.load(open(os.path.join(ROOT, "profiles", "r02b_red_sms.json")))
+            red_peak_s = rs["reds_per_s"]["64MB"][str(NSM)]
+        except Exception:
+            pass
+        if ns and red_peak_s:
+            t_large = sum(v for k, v in ns.items() if "large_" in k)
+            t_step = t_large + sum(v for k, v in ns.items() if "verify_kernel" in k)
+            share_l = t_large / t_step
+            reds = reds_per_even * evens * frac_above
+            ach = reds / ((box_ms / args.steps) / 1e3 * share_l)
+            roofline["klarge"] = {
+                "bound": "l2_red", "achieved": ach / 1e9, "peak": red_peak_s / 1e9, "unit": "G red/s",
+                "frac": ach / red_peak_s, "est_share_of_step": share_l,
+                "kernel": "large_mark_wheel_kernel (+ large_fill_kernel)",
+                "reds_per_even": round(reds_per_even, 5),
+                "basis": (f"2 x {KLARGE_DENSITY:.4f} (cofactors coprime to 2..19) x sum 1/p over "
+                          f"{KLARGE_PRIME_MIN} < p <= {sqrt_hi} red.global.and per even n above 2^42; share "
+                          f"{share_l:.3f} of the step's GPU time from {ls_src}"),
+                "peak_basis": "red.global.and into a 64 MB (L2-resident) buffer from all 148 SMs, "
+                              "profiles/r02b_red_sms.json (scripts/micro/red_sms.cu; 96 MB: 1.28e11/s)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -314,8 +314,11 @@ constexpr int kLargeGridPerSm = 64;
 // multiple whose cofactor k has a factor 5, 7, 11, 13, 17 or 19 is cleared anyway
 // (k even or divisible by 3 puts q outside classes A/B).  Each thread walks its
 // prime's cofactors k >= max(p, q_lo / p) over the residues coprime to 210 and skips
-// k divisible by 11..19 (incremental residues): 17% of the multiples instead of
-// 33%, i.e. about half the L2 atomics of large_mark_kernel.
+// k divisible by 11..19 (a bitmap of k mod 11*13*17*19 in shared memory): 17% of the
+// multiples instead of 33%, i.e. about half the L2 atomics of a plain walk.  The
+// kernel is bound by those atomics: red.global.and runs at ~0.92 per clock per SM
+// and saturates the L2 at ~1.8e11/s from ~100 SMs (64 MB buffer; 1.3e11/s at 96 MB,
+// profiles/r02b_red_sms.json), against 1.15e8 REDs per 3-tile-per-SM chunk at 4e18.
 struct Wheel210 {
     uint8_t res[48];                      // residues mod 210 coprime to 210, ascending
     uint8_t gap[48];                      // gap to the next residue (wrapping)
@@ -333,10 +336,29 @@ constexpr Wheel210 kW210 = make_wheel210();
 static_assert(kW210.res[0] == 1 && kW210.res[47] == 209 && kW210.gap[47] == 2, "wheel 210");
 __constant__ Wheel210 c_w210 = make_wheel210();
 
+// k coprime to 11 * 13 * 17 * 19 = 46189, as a bitmap of k mod 46189 (5.8 KB):
+// one residue register, one shared load and a bit test per cofactor step instead of
+// four incremental residues and their tests
+constexpr uint32_t kM4 = 11u * 13 * 17 * 19;
+constexpr uint32_t kM4Words = (kM4 + 31) / 32;
+struct CopBits {
+    uint32_t w[kM4Words];
+};
+constexpr CopBits make_cop_bits()
+{
+    CopBits b{};
+    for (uint32_t r = 0; r < kM4; ++r)
+        if (r % 11 && r % 13 && r % 17 && r % 19) b.w[r >> 5] |= 1u << (r & 31);
+    return b;
+}
+__device__ const CopBits g_cop = make_cop_bits();
+
 __global__ void __launch_bounds__(kLargeBlock) large_mark_wheel_kernel(LargeArgs a)
 {
     __shared__ uint8_t s_next[210];       // index of the first wheel residue >= r
     __shared__ uint8_t s_res[48], s_gap[48];
+    __shared__ uint32_t s_cop[kM4Words];
+    for (uint32_t i = threadIdx.x; i < kM4Words; i += blockDim.x) s_cop[i] = g_cop.w[i];
     for (int i = threadIdx.x; i < 48; i += blockDim.x) {
         s_res[i] = c_w210.res[i];
         s_gap[i] = c_w210.gap[i];
@@ -382,21 +404,18 @@ __global__ void __launch_bounds__(kLargeBlock) large_mark_wheel_kernel(LargeArgs
         uint64_t off = p * k - q_base;
         if (off >= lim_off) continue;
         const uint32_t kk = km + adv;                     // k mod kM, possibly + up to 10
-        uint32_t r11 = kk % 11, r13 = kk % 13, r17 = kk % 17, r19 = kk % 19;
+        uint32_t r = kk % kM4;
         while (off < lim_off) {
             const uint32_t o = (uint32_t)off;
             const uint32_t m = __umulhi(o, 0xAAAAAAABu) >> 2;     // o / 6
-            if (r11 && r13 && r17 && r19) {
+            if ((s_cop[r >> 5] >> (r & 31)) & 1u) {
                 uint32_t *w = (o - 6 * m == 1 ? mA : mB) + (m >> 5);
                 gmem_and(w, clear_mask(m), pol);
             }
             const uint32_t g = s_gap[idx];
             idx = idx == 47 ? 0 : idx + 1;
             off += p * g;
-            r11 += g; if (r11 >= 11) r11 -= 11;
-            r13 += g; if (r13 >= 13) r13 -= 13;
-            r17 += g; if (r17 >= 17) r17 -= 17;
-            r19 += g; if (r19 >= 19) r19 -= 19;
+            r += g; if (r >= kM4) r -= kM4;
         }
     }
 }

@@ -47,7 +47,7 @@ __host__ __device__ constexpr Trans trans(int a, uint32_t p)
     return b == 5 ? Trans{1, 1, j + 1} : Trans{0, 0, 0};
 }
 
-constexpr int kK = 192;          // unrolled candidates per class
+constexpr int kK = 224;          // unrolled candidates per class (96 / 128 / 192 / 256: slower at 4e18)
 constexpr int kP1 = 56;          // phase 1: candidates every word goes through
 constexpr uint32_t kWinSlack = kWinSlackWords;   // words past a window phase-1 lanes may read (U = 0)
 constexpr int kQueue = kQueueEntries;   // per-warp survivor queue (<= 31 carried + 32 kW per round)
@@ -153,6 +153,15 @@ __device__ __forceinline__ uint32_t class_b_off(uint32_t oa, uint4 k)
     return ob >= k.x ? ob - k.x : ob;
 }
 
+// first hits of a steady prime (p^2 below the window) by one modulo of m_lo: the
+// offsets (rA - m_lo) mod p and (rB - m_lo) mod p (the carry-free path)
+__device__ __forceinline__ void steady_first(uint4 k, int64_t m_lo, uint64_t magic, uint32_t &oa, uint32_t &ob)
+{
+    const uint32_t rem = mod_magic((uint64_t)m_lo, k.x, magic);
+    oa = k.z >= rem ? k.z - rem : k.z + k.x - rem;
+    ob = k.w >= rem ? k.w - rem : k.w + k.x - rem;
+}
+
 // next tile's first hit (the window moves up by tile_m)
 __device__ __forceinline__ uint32_t next_off6(uint32_t off, uint32_t p, uint32_t tm, uint32_t tile_m)
 {
@@ -220,7 +229,7 @@ __device__ __forceinline__ void carry_st(uint32_t *p, uint32_t v, uint64_t pol)
 
 
 // K-SIEVE of one tile's two class windows by the whole CTA; ends WITHOUT a barrier
-template <bool DEF_TILE>
+template <bool DEF_TILE, int KB = 2, int KB2 = 2, bool NOCARRY = false>
 __device__ __forceinline__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
                               Carry6 *cy, const MedSched &ms, uint32_t i_b2, uint32_t i_b1,
                               const uint32_t *__restrict__ lm, int64_t lg0, uint64_t lstride, int tid)
@@ -228,7 +237,7 @@ __device__ __forceinline__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_
     const uint32_t lane = (uint32_t)tid & 31;
     constexpr int nt = kThreads;
     const uint32_t sA = smem_addr(wA), sB = smem_addr(wB);
-    if (cy->init) {
+    if (!NOCARRY && cy->init) {
         // first tile of this CTA's run: carried offsets of the steady primes by modulo
         const int64_t m_lo0 = g0 * 32, m_hi0 = (g0 + (int64_t)nw) * 32;
         const uint64_t ipol = carry_policy();
@@ -306,8 +315,8 @@ __device__ __forceinline__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_
     for (uint32_t pi = sp.i_med + tid; pi < m_end; pi += nt) {
         const uint4 k = __ldg(sp.pk + pi);        // p, kTileM mod p, rA, rB
         uint32_t oa = 0xFFFFFFFFu, ob = 0xFFFFFFFFu;
-        const bool carried = pi < cy->n_carry;
-        if (pi < ns) {
+        const bool carried = !NOCARRY && pi < cy->n_carry;
+        if (!NOCARRY && pi < ns) {
             oa = cy->off[pi];
             ob = cy->off[cy->stride + pi];
             const uint32_t tm = tile_mod<DEF_TILE>(cy, k);
@@ -360,7 +369,7 @@ __device__ __forceinline__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_
     // Steady primes carry only their class-A offset: both progressions step by the
     // same p per tile, so ob = oa + (rB - rA) mod p (both offsets are residues in
     // [0, p) once p^2 lies below the window) -- half the carry-row traffic.
-    constexpr int kB = 2;             // steady primes in flight per thread (1 or 4: slower)
+    constexpr int kB = KB;            // steady primes in flight per thread (1 or 4: slower)
     // steady primes with p <= full window / 2: hit loops (>= 2 hits per class)
     for (uint32_t w0 = b_begin + (tid & ~31u); w0 < b2; w0 += kB * nt) {   // warp-uniform trips
         const uint32_t p0 = w0 + lane;
@@ -371,9 +380,14 @@ __device__ __forceinline__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_
             const uint32_t pi = p0 + k * nt;
             if (pi < b2) {
                 const uint4 q = __ldg(pkp + pi);
-                pt[k] = make_uint2(q.x, tile_mod<DEF_TILE>(cy, q));
-                oa[k] = carry_ld(cA + pi, cpol);
-                ob[k] = class_b_off(oa[k], q);
+                if constexpr (NOCARRY) {
+                    pt[k] = make_uint2(q.x, 0);
+                    steady_first(q, m_lo, __ldg(sp.magic + pi), oa[k], ob[k]);
+                } else {
+                    pt[k] = make_uint2(q.x, tile_mod<DEF_TILE>(cy, q));
+                    oa[k] = carry_ld(cA + pi, cpol);
+                    ob[k] = class_b_off(oa[k], q);
+                }
             } else {
                 pt[k] = make_uint2(1, 0);
                 oa[k] = ob[k] = nbits;
@@ -398,12 +412,13 @@ __device__ __forceinline__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_
                 for (; bb < nbits; bb += p) clear_bit(sB, bb);
             }
             const uint32_t pi = p0 + k * nt;
-            if (pi < b2) carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
+            if (!NOCARRY && pi < b2) carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
         }
         __syncwarp();   // reconverge: the per-lane hit loops diverge
     }
     // steady primes with window/2 < p <= window: at most 2 hits per class, predicated
-    constexpr int kB2 = 2;            // primes in flight per thread (4: -1% at 1e12, +1.4% at 4e18; 8: slower)
+    constexpr int kB2 = KB2;          // primes in flight per thread: 4 in the out-of-line sieve (below 2^42:
+                                      // 29.07 vs 29.34 ms), 2 inlined (4: +1.4% at 4e18; 8: slower)
     for (uint32_t w0 = b2 + (tid & ~31u); w0 < b1; w0 += kB2 * nt) {
         const uint32_t p0 = w0 + lane;
         uint32_t pp[kB2], tt[kB2], oa[kB2], ob[kB2];
@@ -413,9 +428,14 @@ __device__ __forceinline__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_
             if (pi < b1) {
                 const uint4 q = __ldg(pkp + pi);
                 pp[k] = q.x;
-                tt[k] = tile_mod<DEF_TILE>(cy, q);
-                oa[k] = carry_ld(cA + pi, cpol);
-                ob[k] = class_b_off(oa[k], q);
+                if constexpr (NOCARRY) {
+                    tt[k] = 0;
+                    steady_first(q, m_lo, __ldg(sp.magic + pi), oa[k], ob[k]);
+                } else {
+                    tt[k] = tile_mod<DEF_TILE>(cy, q);
+                    oa[k] = carry_ld(cA + pi, cpol);
+                    ob[k] = class_b_off(oa[k], q);
+                }
             } else {
                 pp[k] = nbits; tt[k] = 0;
                 oa[k] = ob[k] = nbits;
@@ -429,7 +449,7 @@ __device__ __forceinline__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_
             if (ob[k] < nbits) clear_bit(sB, ob[k]);
             if (ob[k] + p < nbits) clear_bit(sB, ob[k] + p);
             const uint32_t pi = p0 + k * nt;
-            if (pi < b1) carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
+            if (!NOCARRY && pi < b1) carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
         }
     }
     // steady primes with p > a full window: at most 1 hit per class
@@ -442,9 +462,14 @@ __device__ __forceinline__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_
             if (pi < s_end) {
                 const uint4 q = __ldg(pkp + pi);
                 pp[k] = q.x;
-                tt[k] = tile_mod<DEF_TILE>(cy, q);
-                oa[k] = carry_ld(cA + pi, cpol);
-                ob[k] = class_b_off(oa[k], q);
+                if constexpr (NOCARRY) {
+                    tt[k] = 0;
+                    steady_first(q, m_lo, __ldg(sp.magic + pi), oa[k], ob[k]);
+                } else {
+                    tt[k] = tile_mod<DEF_TILE>(cy, q);
+                    oa[k] = carry_ld(cA + pi, cpol);
+                    ob[k] = class_b_off(oa[k], q);
+                }
             } else {
                 pp[k] = nbits; tt[k] = 0;
                 oa[k] = ob[k] = nbits;
@@ -456,14 +481,14 @@ __device__ __forceinline__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_
             if (oa[k] < nbits) clear_bit(sA, oa[k]);
             if (ob[k] < nbits) clear_bit(sB, ob[k]);
             const uint32_t pi = p0 + k * nt;
-            if (pi < s_end) carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
+            if (!NOCARRY && pi < s_end) carry_st(cA + pi, oa[k] >= tm ? oa[k] - tm : oa[k] + p - tm, cpol);
         }
     }
     for (uint32_t pi = s_end + tid; pi < sp.n_use; pi += nt) {
         const uint4 k = __ldg(sp.pk + pi);
         const int64_t mmin = (int64_t)(((uint64_t)k.x * k.x - 1) / 6);
         if (mmin >= m_hi) break;
-        const bool carried = pi < cy->n_carry;
+        const bool carried = !NOCARRY && pi < cy->n_carry;
         uint32_t oa, ob;
         if (carried && cy->have_prev && mmin < m_hi - (int64_t)cy->tile_m) {
             oa = cy->off[pi];
@@ -491,15 +516,18 @@ __device__ __noinline__ void sieve6_window_call(uint32_t *wA, uint32_t *wB, int6
                                                 uint32_t i_b2, uint32_t i_b1, const uint32_t *__restrict__ lm,
                                                 int64_t lg0, uint64_t lstride, int tid)
 {
-    sieve6_window<DEF_TILE>(wA, wB, g0, nw, sp, cy, ms, i_b2, i_b1, lm, lg0, lstride, tid);
+    sieve6_window<DEF_TILE, 2, 4>(wA, wB, g0, nw, sp, cy, ms, i_b2, i_b1, lm, lg0, lstride, tid);
 }
+#ifndef GB_NOCARRY_INL
+#define GB_NOCARRY_INL false
+#endif
 template <bool DEF_TILE, bool OUTLINE>
 __device__ __forceinline__ void sieve6(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
                                        Carry6 *cy, const MedSched &ms, uint32_t i_b2, uint32_t i_b1,
                                        const uint32_t *__restrict__ lm, int64_t lg0, uint64_t lstride, int tid)
 {
     if constexpr (OUTLINE) sieve6_window_call<DEF_TILE>(wA, wB, g0, nw, sp, cy, ms, i_b2, i_b1, lm, lg0, lstride, tid);
-    else sieve6_window<DEF_TILE>(wA, wB, g0, nw, sp, cy, ms, i_b2, i_b1, lm, lg0, lstride, tid);
+    else sieve6_window<DEF_TILE, 2, 2, GB_NOCARRY_INL>(wA, wB, g0, nw, sp, cy, ms, i_b2, i_b1, lm, lg0, lstride, tid);
 }
 
 // ---------------------------------------------------------------------------
@@ -1005,6 +1033,7 @@ extern __shared__ uint32_t g_win[];
 struct Shared6 {
     uint32_t hist[kHistSmem];          // bins by prime index (runtime loop, fallback, specials)
     uint32_t histc[3][kK + 1];         // per class: [0] evens entering the table, [J + 1] = A_J (hist8)
+    uint32_t wint[kMarkWarps][3];      // per warp and class: interior rounds of this tile (no atomics)
     uint32_t next_round[2];            // per window slot
     uint32_t ns[2];
     uint32_t q_base;      // word offset of the queues in dynamic shared memory
@@ -1091,10 +1120,7 @@ struct ClassWork {
                 m.U[k] = FULL;
                 if (TRACK) { m.lb[k] = 0; m.lu[k] = 0; }
             }
-            if (lane == 0) {                                 // evens of the round, all entering the table
-                atomicAdd(&sh.histc[A / 2][0], 32u * 32u * kW);
-                atomicAdd(&acc->evens, 32ull * 32ull * kW);
-            }
+            if (lane == 0) sh.wint[warp][A / 2] += 1;       // warp-private: folded in at the tile flush
         } else {
             uint32_t c = 0, e = 0;
 #pragma unroll
@@ -1331,6 +1357,7 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant_
     if (tid == 0) sh.q_base = 2 * nw_max;
     for (int i = tid; i < kHistSmem; i += kThreads) sh.hist[i] = 0;
     for (int i = tid; i < 3 * (kK + 1); i += kThreads) (&sh.histc[0][0])[i] = 0;
+    for (int i = tid; i < 3 * kMarkWarps; i += kThreads) (&sh.wint[0][0])[i] = 0;
     if (tid == 0) sh.acc = CtaAcc{0, 0, 0, 0, 0, ~0ull, 0};
     CtaAcc *const acc = &sh.acc;
     uint32_t best_p = 0;                       // per warp: replay only blocks that can raise the max
@@ -1376,6 +1403,13 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant_
         mark_tile<DUMP, UNROLL, INB>(sh, sh.next_round[0], u0, tw, wA, wB, halo, a, acc, best_p, lane, warp);
         // per-tile flush of the shared histograms keeps their 32-bit bins exact
         __syncthreads();
+        if (tid < 3) {                 // interior rounds: 32 kW words of 32 live evens each
+            uint32_t n = 0;
+            for (int w = 0; w < kMarkWarps; ++w) { n += sh.wint[w][tid]; sh.wint[w][tid] = 0; }
+            sh.histc[tid][0] += n * 32u * 32u * kW;
+            if (n) atomicAdd(&acc->evens, (unsigned long long)n * 32ull * 32ull * kW);
+        }
+        __syncthreads();
         flush_hist(sh, a, acc, tid);
     }
     // the CTA's counts (thread 0) and the max key (one atomic per warp)
@@ -1402,6 +1436,12 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant_
 // (class B) is o = 3m + 1: the 96 odd bits [96g, 96g+96) hold B bits 32g..32g+31 at
 // o = 96g + 3j + 1 and A bits 32g+1..32g+32 at o = 96g + 3j + 2.
 // ---------------------------------------------------------------------------
+#ifndef GB_SO_KB
+#define GB_SO_KB 2
+#endif
+#ifndef GB_SO_KB2
+#define GB_SO_KB2 2
+#endif
 __global__ void __launch_bounds__(kThreads) sieve_out_kernel(const __grid_constant__ SieveOutArgs a)
 {
     uint32_t *win = g_win;
@@ -1435,10 +1475,10 @@ __global__ void __launch_bounds__(kThreads) sieve_out_kernel(const __grid_consta
         cy.n_steady = sh_ns & 0x7FFFFFFFu;
         cy.init = sh_ns >> 31;
         if (cy.tile_m == kTileM)
-            sieve6_window<true>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
+            sieve6_window<true, GB_SO_KB, GB_SO_KB2>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
                                 a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride, tid);
         else
-            sieve6_window<false>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
+            sieve6_window<false, GB_SO_KB, GB_SO_KB2>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
                                  a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride, tid);
         cy.have_prev = true;
         __syncthreads();

@@ -18,9 +18,10 @@ ap.add_argument("--span", type=int, default=36)
 ap.add_argument("--N", default="1e12")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--rounds", type=int, default=2)
+ap.add_argument("--abdir", default="ab", help="directory of the A/B builds")
 ap.add_argument("--hi", default=None, help="exclusive top of the range (e.g. 4000000000000000000 for C5)")
 a = ap.parse_args()
-libs = [os.path.join(ROOT, "paper_2603_02621_b200", "libgb.so")] + sorted(glob.glob(os.path.join(ROOT, "ab", "*.so")))
+libs = [os.path.join(ROOT, "paper_2603_02621_b200", "libgb.so")] + sorted(glob.glob(os.path.join(ROOT, a.abdir, "*.so")))
 for rnd in range(a.rounds):
     for lib in libs:
         env = dict(os.environ, GB_LIB=lib)

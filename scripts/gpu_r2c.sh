@@ -49,6 +49,7 @@ for w in $what; do
       # verify report is kept: gpurun copies back at most 64 MiB
       $F -k regex:verify_kernel -o gpurun_out/prof_verify_c4 python scripts/prof_one.py --span 36 > gpurun_out/prof_c4.log 2>&1
       echo "ncu verify c4 rc=$?"
+      python scripts/ncu_regions.py gpurun_out/prof_verify_c4.ncu-rep > gpurun_out/regions_verify_c4.txt 2>&1
       $S gpurun_out/prof_verify_c4.ncu-rep gpurun_out/sum_verify_kernel_c4 --evens 34359738368 \
         --note "ncu --set full --clock-control none, one gb_verify_range over the top 2^36 integers of [4, 1e12] (scripts/prof_one.py --span 36)" > /dev/null
       $F -k regex:sieve_out -o gpurun_out/prof_sieve_c4 python scripts/prof_one.py --span 34 > /dev/null 2>&1
@@ -60,6 +61,7 @@ for w in $what; do
       echo "ncu verify c5 rc=$?"
       $S gpurun_out/prof_verify_c5.ncu-rep gpurun_out/sum_verify_kernel_c5 --evens 872939520 \
         --note "ncu --set full, the first verify launch (one K-LARGE chunk: 444 tiles = 8.73e8 evens) of the top 2^34 integers of [4e18 - 1e11, 4e18)" > /dev/null
+      python scripts/ncu_regions.py gpurun_out/prof_verify_c5.ncu-rep > gpurun_out/regions_verify_c5.txt 2>&1
       rm -f gpurun_out/prof_verify_c5.ncu-rep
       $F -k regex:large_mark -o gpurun_out/prof_large_c5 python scripts/prof_one.py --hi 4000000000000000000 --span 34 > /dev/null 2>&1
       echo "ncu large c5 rc=$?"
