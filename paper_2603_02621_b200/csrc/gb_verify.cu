@@ -509,25 +509,24 @@ __device__ __forceinline__ void sieve6_window(uint32_t *wA, uint32_t *wB, int64_
 
 // The sieve as its own function (own register allocation, called once per tile):
 // below 2^42 the marking code then compiles without the sieve's pressure (29.31 vs
-// 29.51 ms at 1e12); in the K-LARGE regime inlined (93.05 vs 93.76 ms at 4e18).
+// 29.51 ms at 1e12); in the K-LARGE regime inlined (93.05 vs 93.76 ms at 4e18) and
+// carry-free (steady offsets by modulo per tile: 84.6 vs 90.5 ms; below 2^42 the
+// carry rows stay L2-resident and win, 29.0 vs 29.9 ms).
 template <bool DEF_TILE>
 __device__ __noinline__ void sieve6_window_call(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw,
                                                 const SievePrimes &sp, Carry6 *cy, const MedSched &ms,
                                                 uint32_t i_b2, uint32_t i_b1, const uint32_t *__restrict__ lm,
                                                 int64_t lg0, uint64_t lstride, int tid)
 {
-    sieve6_window<DEF_TILE, 2, 4>(wA, wB, g0, nw, sp, cy, ms, i_b2, i_b1, lm, lg0, lstride, tid);
+    sieve6_window<DEF_TILE, 2, 4, false>(wA, wB, g0, nw, sp, cy, ms, i_b2, i_b1, lm, lg0, lstride, tid);
 }
-#ifndef GB_NOCARRY_INL
-#define GB_NOCARRY_INL false
-#endif
 template <bool DEF_TILE, bool OUTLINE>
 __device__ __forceinline__ void sieve6(uint32_t *wA, uint32_t *wB, int64_t g0, uint32_t nw, const SievePrimes &sp,
                                        Carry6 *cy, const MedSched &ms, uint32_t i_b2, uint32_t i_b1,
                                        const uint32_t *__restrict__ lm, int64_t lg0, uint64_t lstride, int tid)
 {
     if constexpr (OUTLINE) sieve6_window_call<DEF_TILE>(wA, wB, g0, nw, sp, cy, ms, i_b2, i_b1, lm, lg0, lstride, tid);
-    else sieve6_window<DEF_TILE, 2, 2, GB_NOCARRY_INL>(wA, wB, g0, nw, sp, cy, ms, i_b2, i_b1, lm, lg0, lstride, tid);
+    else sieve6_window<DEF_TILE, 2, 2, true>(wA, wB, g0, nw, sp, cy, ms, i_b2, i_b1, lm, lg0, lstride, tid);
 }
 
 // ---------------------------------------------------------------------------
@@ -1436,12 +1435,6 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(const __grid_constant_
 // (class B) is o = 3m + 1: the 96 odd bits [96g, 96g+96) hold B bits 32g..32g+31 at
 // o = 96g + 3j + 1 and A bits 32g+1..32g+32 at o = 96g + 3j + 2.
 // ---------------------------------------------------------------------------
-#ifndef GB_SO_KB
-#define GB_SO_KB 2
-#endif
-#ifndef GB_SO_KB2
-#define GB_SO_KB2 2
-#endif
 __global__ void __launch_bounds__(kThreads) sieve_out_kernel(const __grid_constant__ SieveOutArgs a)
 {
     uint32_t *win = g_win;
@@ -1475,10 +1468,10 @@ __global__ void __launch_bounds__(kThreads) sieve_out_kernel(const __grid_consta
         cy.n_steady = sh_ns & 0x7FFFFFFFu;
         cy.init = sh_ns >> 31;
         if (cy.tile_m == kTileM)
-            sieve6_window<true, GB_SO_KB, GB_SO_KB2>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
+            sieve6_window<true, 2, 4>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
                                 a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride, tid);
         else
-            sieve6_window<false, GB_SO_KB, GB_SO_KB2>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
+            sieve6_window<false, 2, 4>(wA, wB, (int64_t)g0, tw + 1, a.sp, &cy, MedSched{a.med_idx, a.med_off}, a.i_b2,
                                  a.i_b1, a.lmask, a.lmask_g0, a.lmask_stride, tid);
         cy.have_prev = true;
         __syncthreads();
