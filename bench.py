@@ -65,17 +65,29 @@ def parse():
                          "(default N = 1e9; NEXT-4, PAPER.md:421)")
     ap.add_argument("--counts-window", type=int, default=16384, help="even n per step in --mode counts")
     ap.add_argument("--strips-per-rank", type=int, default=None,
-                    help="default 8 (balances the growth of work with n); 2 for c5 (the window's cost "
-                         "is flat; fewer partial K-LARGE chunks)")
+                    help="default 8 (balances the growth of work with n), fewer when a strip would have "
+                         "under 8 tiles per SM; 2 for c5 (the window's cost is flat; fewer partial "
+                         "K-LARGE chunks)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sieve", action="store_true", help="skip the standalone sieve GB/s leg")
     ap.add_argument("--no-check", action="store_true", help="do not exit 1 on a failed result check")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     a = ap.parse_args()
-    if a.strips_per_rank is None:
-        a.strips_per_rank = 2 if a.workload == "c5" and a.N is None else 8
     return a
+
+
+def auto_strips(args, lo: int, hi: int, world: int) -> int:
+    """Strips (one gb_verify_range each) per rank: 2 for the C5 window (flat cost, fewer
+    partial K-LARGE chunks); else 8 (balances the growth of work with n), but never
+    fewer than 8 tiles per SM in a strip: a small range ([4, 1e9] is 254 tiles) runs as
+    one call, whose tiles libgb balances over the SMs."""
+    if args.strips_per_rank is not None:
+        return args.strips_per_rank
+    if args.workload == "c5" and args.N is None:
+        return 2
+    tiles = (hi - lo) / (192 * 20480) / world          # 192 integers per class word
+    return max(1, min(8, int(tiles // (8 * NSM))))
 
 
 def workload(args):
@@ -441,6 +453,7 @@ def main():
     # resident mode sieves every word of [3, hi): the context must cover their top q
     hi_max = max(hi, 3 + 128 * n_bits_words) if n_bits_words else hi
     V = Verifier(hi_max=hi_max, p_max=args.p_max, origin=origin, device=local, stream=stream)
+    args.strips_per_rank = auto_strips(args, lo, hi, world)
     strips = gdist.rank_strips(gdist.plan_strips(lo, hi, args.strips_per_rank * world), rank, world)
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(4 * l2_bytes, 1 << 28) // 4, dtype=torch.int32, device=dev)

@@ -464,6 +464,21 @@ gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_m
     const size_t smem = verify_smem(a.halo);
     const int per_sm = verify_blocks_per_sm(smem);
     const uint64_t max_grid = (uint64_t)per_sm * ctx->num_sms;
+    {
+        // a few tiles per CTA (small ranges): shrink the tile so that every CTA gets
+        // the same number of whole tiles (e.g. [4, 1e9]: 254 default tiles on 148
+        // CTAs, 106 of them doing two -> 296 tiles of 17,664 words, two each)
+        const uint64_t gmax = std::min<uint64_t>(max_grid, ctx->carry_ctas);
+        const uint64_t words = a.u_end - a.u_first;
+        if (gmax > 0 && a.n_tiles > gmax && a.n_tiles < 8 * gmax) {
+            const uint64_t per = (a.n_tiles + gmax - 1) / gmax;
+            const uint64_t tw = ((words + per * gmax - 1) / (per * gmax) + 127) & ~127ull;
+            if (tw < a.tile_words) {
+                a.tile_words = (uint32_t)tw;
+                a.n_tiles = (words + tw - 1) / tw;
+            }
+        }
+    }
     const int grid = (int)std::min<uint64_t>(std::min<uint64_t>(a.n_tiles, max_grid), ctx->carry_ctas);
     a.carry = ctx->carry;
     a.carry_stride = ctx->carry_stride;
