@@ -29,6 +29,7 @@ uint64_t isqrt_u64(uint64_t x)
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 constexpr uint64_t kMaxSms = 160;   // workspace sizing bound (B200: 148)
+constexpr uint64_t kMinTileWords = 1024;   // smallest balanced tile (and never below the halo)
 
 struct Layout {
     uint64_t R, bits_words, list_cap, n_blk, carry_stride, carry_ctas, lmask_stride;
@@ -468,11 +469,13 @@ gb_status gb_verify_range_ex(gb_ctx *ctx, uint64_t lo, uint64_t hi, uint32_t p_m
         // a few tiles per CTA (small ranges): shrink the tile so that every CTA gets
         // the same number of whole tiles (e.g. [4, 1e9]: 254 default tiles on 148
         // CTAs, 106 of them doing two -> 296 tiles of 17,664 words, two each)
+        // (fewer tiles than CTAs: tiles of at least kMinTileWords, one per CTA)
         const uint64_t gmax = std::min<uint64_t>(max_grid, ctx->carry_ctas);
         const uint64_t words = a.u_end - a.u_first;
-        if (gmax > 0 && a.n_tiles > gmax && a.n_tiles < 8 * gmax) {
+        if (gmax > 0 && a.n_tiles < 8 * gmax) {
             const uint64_t per = (a.n_tiles + gmax - 1) / gmax;
-            const uint64_t tw = ((words + per * gmax - 1) / (per * gmax) + 127) & ~127ull;
+            uint64_t tw = ((words + per * gmax - 1) / (per * gmax) + 127) & ~127ull;
+            tw = std::max<uint64_t>(tw, std::max<uint64_t>(kMinTileWords, a.halo));   // re-sieved halo <= tile
             if (tw < a.tile_words) {
                 a.tile_words = (uint32_t)tw;
                 a.n_tiles = (words + tw - 1) / tw;
