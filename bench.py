@@ -86,7 +86,7 @@ def auto_strips(args, lo: int, hi: int, world: int) -> int:
         return args.strips_per_rank
     if args.workload == "c5" and args.N is None:
         return 2
-    tiles = (hi - lo) / (192 * 20480) / world          # 192 integers per class word
+    tiles = (hi - lo) / (192 * 21376) / world          # 192 integers per class word, kTileWords
     return max(1, min(8, int(tiles // (8 * NSM))))
 
 
