@@ -48,10 +48,11 @@ __host__ __device__ constexpr Trans trans(int a, uint32_t p)
 }
 
 constexpr int kK = 224;          // unrolled candidates per class (96 / 128 / 192 / 256: slower at 4e18)
-constexpr int kP1 = 56;          // phase 1: candidates every word goes through
+constexpr int kP1 = 56;          // phase 1: candidates every word goes through (48 / 64: slower at 1e12)
+constexpr int kP1L = 64;         // the same in the K-LARGE regime (56: 1.9% slower at 4e18, 48: 3.7%)
 constexpr uint32_t kWinSlack = kWinSlackWords;   // words past a window phase-1 lanes may read (U = 0)
 constexpr int kQueue = kQueueEntries;   // per-warp survivor queue (<= 31 carried + 32 kW per round)
-static_assert(kK % 8 == 0 && kP1 % 8 == 0 && kP1 <= kK, "blocks of 8 candidates");
+static_assert(kK % 8 == 0 && kP1 % 8 == 0 && kP1 <= kK && kP1L % 8 == 0 && kP1L <= kK, "blocks of 8 candidates");
 
 
 struct ClassTable {
@@ -708,8 +709,9 @@ __device__ __forceinline__ void phase1q(LaneQ &m, uint32_t *h, int lane)
 // words per lane (a round's survivors gathered through the warp's queue area), so
 // candidates kC1 .. kP1-1 run only on live words.  Word k of a lane has its own
 // window position li[k].
-constexpr int kC1 = 40;          // compaction point (24/32/48: slower)
-static_assert(kC1 % 8 == 0 && kC1 <= kP1, "compaction point on a block boundary");
+constexpr int kC1 = 32;          // compaction point (40: +0.3% at 1e12; 24 / 48: slower)
+constexpr int kC1L = 40;         // the same in the K-LARGE regime (32: +4.9% at 4e18, 48: +1.0%)
+static_assert(kC1 % 8 == 0 && kC1 <= kP1 && kC1L % 8 == 0 && kC1L <= kP1L, "compaction point on a block boundary");
 
 template <int S>
 struct LaneR {
@@ -774,12 +776,12 @@ __device__ __forceinline__ void block8r(LaneR<S> &m, uint32_t *h, int lane)
     hist8(c0, c1, c2, c3, c4, c5, c6, c7, h + J, lane);
 }
 
-template <int A, int J, int S, bool DUMP, bool TRACK>
+template <int A, int J, int JEND, int S, bool DUMP, bool TRACK>
 __device__ __forceinline__ void phase1r(LaneR<S> &m, uint32_t *h, int lane)
 {
-    if constexpr (J < kP1) {
+    if constexpr (J < JEND) {
         block8r<A, J, S, DUMP, TRACK>(m, h, lane);
-        phase1r<A, J + 8, S, DUMP, TRACK>(m, h, lane);
+        phase1r<A, J + 8, JEND, S, DUMP, TRACK>(m, h, lane);
     }
 }
 
@@ -1050,6 +1052,8 @@ __device__ __forceinline__ uint16_t *sh_qli(const Shared6 &sh, int warp)
 
 template <int A, bool DUMP, bool UNROLL, bool INB>
 struct ClassWork {
+    static constexpr int P1 = INB ? kP1L : kP1;     // phase-1 length and compaction point of this regime
+    static constexpr int C1 = INB ? kC1L : kC1;
     // one phase-2 batch of `take` queued words of class A (out of line: called from
     // the round loop and the queue flushes; keeps the hot code small)
     // (everything by value: no local-memory round trip of the caller's state; the
@@ -1071,7 +1075,7 @@ struct ClassWork {
         m.U = U;
         m.lb = 0; m.lu = 0;
         m.dump_w = DUMP ? a.dump + ((int64_t)(192 * u + A) - (int64_t)a.lo_e) / 2 : nullptr;
-        phase2<A, kP1, DUMP>(m, sh.histc[A / 2] + 1, lane);
+        phase2<A, P1, DUMP>(m, sh.histc[A / 2] + 1, lane);
         replay_key<A>(m, u, a, best_p, acc);
         constexpr uint32_t j_next = kTab[A / 2].bin[kK - 1] - 1;   // odd-list index after the table
         finish_word<A, DUMP>(m.U, j_next, m.wa, m.wb, u, sh.hist, a, acc, lane);
@@ -1138,7 +1142,7 @@ struct ClassWork {
                 atomicAdd(&acc->evens, (unsigned long long)(c >> 16));
             }
         }
-        phase1q<A, 0, kC1, DUMP, TRACK>(m, sh.histc[A / 2] + 1, lane);
+        phase1q<A, 0, C1, DUMP, TRACK>(m, sh.histc[A / 2] + 1, lane);
         if (TRACK) replay_key_q<A>(m, u0 + li0, a, best_p, acc);
         // survivors of candidates [0, kC1): staged past the queue's live entries,
         // then compacted to 2 (or 1) words per lane for candidates [kC1, kP1)
@@ -1190,7 +1194,7 @@ struct ClassWork {
             if (DUMP) m.dump[k] = a.dump + ((int64_t)(192 * (u0 + li) + A) - (int64_t)a.lo_e) / 2;
         }
         __syncwarp();                          // staged entries read before any append
-        phase1r<A, kC1, S, DUMP, TRACK>(m, sh.histc[A / 2] + 1, lane);
+        phase1r<A, C1, P1, S, DUMP, TRACK>(m, sh.histc[A / 2] + 1, lane);
         if (TRACK) replay_key_r<A, S>(m, u0, a, best_p, acc);
 #pragma unroll
         for (int k = 0; k < S; ++k) {
@@ -1212,7 +1216,7 @@ struct ClassWork {
     {
         if constexpr (UNROLL) {
             // max-key tracking only while phase-1 primes can still raise this warp's max
-            constexpr uint32_t kP1Max = kTab[A / 2].p[kP1 - 1];
+            constexpr uint32_t kP1Max = kTab[A / 2].p[P1 - 1];
             if (best_p > kP1Max)
                 round_q<false>(sh, qn, pair, tw, u0, wA, wB, halo, a, acc, best_p, lane, warp);
             else
